@@ -1,0 +1,358 @@
+#!/usr/bin/env python3
+"""bench.py -- batched resident-KV-claim arbitration on B200 (BASELINE.json metric:
+allocator events/s and traces/s at 1/2/4/8 GPUs, % of HBM roofline).
+
+One bench step = one pass of the whole hot path over one batch:
+  rkc_pool_reset -> rkc_step_batch(T=256 lockstep steps over 100k traces, ops
+  resident in HBM) -> rkc_telemetry_read (K2 event compaction + K3 outcome
+  histogram, device outputs) -> NCCL allreduce of the histogram (N > 1).
+Workload (config c3, weak scaling): 100,000 random traces per GPU, 1024-block pools,
+T = 256 steps; rank r replays trace ids [r*100k, (r+1)*100k).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+Under torchrun (N > 1) every rank runs; rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "allocator events/sec and traces/sec at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "events/s"
+TRACES, NBLK, TSTEPS, C, Q, O = 100_000, 1024, 256, 16, 16, 64
+EPT = 512
+SEED = 0
+
+
+def workload_config(n_gpus: int) -> dict:
+    return {"workload": "c3: 100k random traces per GPU, 1024-block pools (16-token blocks), "
+                        "T=256 lockstep steps, mixed chunked prefill/decode, 4-16 claims",
+            "traces_per_gpu": TRACES, "pool_blocks": NBLK, "steps_per_replay": TSTEPS,
+            "global_traces": TRACES * n_gpus, "parallelism": f"trace-sharded x{n_gpus}",
+            "l2": "inputs larger than L2: pool state 0.83 GB + ops 0.41 GB per GPU, no flush"}
+
+
+# --------------------------------------------------------------------------
+# algorithmic bytes of the step kernel (DESIGN.md sec. 4 "byte model")
+# --------------------------------------------------------------------------
+def algorithmic_bytes(ops: np.ndarray, counters: np.ndarray, events: np.ndarray) -> dict:
+    """Bytes the method must move in this layout for one full replay.
+
+    per trace-step      : op 16 + hot header 64 (read)
+    per non-NOP op      : header write 64, claim table 32*C, object table 8*O (read)
+    per victim selection: selection keys 4*N + free bitmap N/8 (read),
+                          per taken block 12 (meta gather + meta/key write)
+    per free-only alloc : bitmap N/8, per block 8 (meta/key write)
+    per meta scan       : 4*N (COMPLETE, deferral/refusal release, TOUCH with L>0)
+    per event           : 32 (write)
+    """
+    T, n = ops.shape
+    non_nop = int((ops["kind"] != 0).sum())
+    kinds = events["type"]
+    vic = events[kinds == 12]
+    k_evict = int(vic["f"][:, 3].astype(np.int64).sum())
+    n_evict = len(vic)
+    blocks_alloc = int(counters[:, 21].astype(np.int64).sum())
+    k_free = blocks_alloc - k_evict
+    adv_ins = int(((ops["kind"] == 3) | (ops["kind"] == 5)).sum())
+    served = int((kinds == 11).sum())
+    released = int(((kinds == 7) | (kinds == 8)).sum())
+    touch_scan = int(((kinds == 13) & (events["f"][:, 1] > 0)).sum())
+    n_events = len(events)
+    b = 0
+    b += T * n * (16 + 64)
+    b += non_nop * (64 + 32 * C + 8 * O)
+    b += n_evict * (4 * NBLK + NBLK // 8) + 12 * k_evict
+    b += max(0, adv_ins - n_evict) * (NBLK // 8) + 8 * max(0, k_free)
+    b += (served + released + touch_scan) * 4 * NBLK
+    b += 32 * n_events
+    return dict(bytes=int(b), non_nop=non_nop, evicting_selections=n_evict, events=n_events)
+
+
+# --------------------------------------------------------------------------
+def clocks_sampler(path: str, gpu_index: int):
+    q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    try:
+        return subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={q}",
+                                 "--format=csv,noheader,nounits", "-lms", "200"],
+                                stdout=open(path, "w"), stderr=subprocess.DEVNULL)
+    except Exception:
+        return None
+
+
+def clocks_summary(path: str) -> dict:
+    sm, mx, reasons = [], [], set()
+    try:
+        for line in open(path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                "sw_power_cap"), f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+    except OSError:
+        pass
+    if not sm:
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+    return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+            "samples": len(sm)}
+
+
+def load_peak() -> tuple[float, str]:
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic() -> float | None:
+    """dram bytes per step-kernel launch from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_step_kernel.json")
+    try:
+        return float(json.load(open(p))["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------------
+def cpu_baseline(cfgs, ops, budget_s: float = 12.0) -> dict:
+    """The oracle as it stands, on the host cores, on a bounded sample of the
+    same workload (the first traces of rank 0's shard)."""
+    from oracle import oracle as orc
+    nthreads = os.cpu_count() or 1
+    chunk = max(64, 16 * nthreads)
+    done_traces, ops_done, t_used = 0, 0, 0.0
+    while t_used < budget_s and done_traces < ops.shape[1]:
+        sl = slice(done_traces, min(done_traces + chunk, ops.shape[1]))
+        sub = np.ascontiguousarray(ops[:, sl])
+        b = orc.OracleBatch(cfgs[sl], NBLK, C, Q, O)
+        t0 = time.perf_counter()
+        b.run(sub, nthreads=nthreads)
+        t_used += time.perf_counter() - t0
+        ops_done += int((sub["kind"] != 0).sum())
+        done_traces = sl.stop
+    return {"value": ops_done / t_used, "unit": UNIT, "cores": nthreads, "kind": "oracle",
+            "sample": f"first {done_traces} traces of the c3 workload x {TSTEPS} steps "
+                      f"({ops_done} non-NOP ops) in {t_used:.1f} s, plain C++ oracle (-O2), "
+                      f"{nthreads} threads, one trace per task",
+            "traces_per_s": done_traces / t_used}
+
+
+def run_reference(args, rank: int, world: int):
+    """--impl reference: the oracle, as it stands, on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    from paper_2605_24259_b200 import gen
+    from oracle import oracle as orc
+    nthreads = os.cpu_count() or 1
+    sample = max(64, 32 * nthreads)
+    cfgs, ops = gen.random_traces(3, SEED, 0, sample, TSTEPS, NBLK, C, Q, O)
+    non_nop = int((ops["kind"] != 0).sum())
+    times = []
+    for i in range(args.warmup + args.steps):
+        b = orc.OracleBatch(cfgs, NBLK, C, Q, O)
+        t0 = time.perf_counter()
+        b.run(ops, nthreads=nthreads)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    t = float(np.sum(times))
+    value = non_nop * args.steps / t
+    desc = (f"each step: the first {sample} traces of the c3 workload x {TSTEPS} steps "
+            f"({non_nop} non-NOP ops), plain C++ oracle, {nthreads} threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic", "config": workload_config(world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "oracle",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "traces_per_s": sample * args.steps / t,
+    }), flush=True)
+
+
+# --------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="rkc", choices=["rkc", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2605_24259_b200 import build, gen
+    build.build()
+    from paper_2605_24259_b200 import rkc
+
+    torch.cuda.set_device(local_rank)
+    dist_on = world > 1
+    if dist_on:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+
+    # ---- inputs: this rank's shard, generated on the host, resident in HBM ----
+    cfgs, ops = gen.random_traces(3, SEED, rank * TRACES, TRACES, TSTEPS, NBLK, C, Q, O)
+    non_nop = int((ops["kind"] != 0).sum())
+    ops_u8 = ops.view(np.uint8).reshape(-1)
+    ops_dev = torch.from_numpy(ops_u8).to(dev)
+    ops_pinned = torch.empty(ops_u8.size, dtype=torch.uint8, pin_memory=True)
+    ops_pinned.numpy()[:] = ops_u8
+    pool = rkc.Pool(cfgs, NBLK, C, Q, O, events_per_trace=EPT, device=local_rank)
+    stream = torch.cuda.current_stream(dev)
+    ev_cap = TRACES * EPT
+    events_dev = torch.empty(ev_cap * 32, dtype=torch.uint8, device=dev)
+    hist_dev = torch.zeros(rkc.RKC_NHIST, dtype=torch.int64, device=dev)
+
+    def one_step(ev_pair=None):
+        pool.rkc_pool_reset(stream)
+        if ev_pair is not None:
+            ev_pair[0].record(stream)
+        pool.rkc_step_batch(ops_dev, TSTEPS, stream)
+        if ev_pair is not None:
+            ev_pair[1].record(stream)
+        pool.rkc_telemetry_read(events_out=events_dev, hist_out=hist_dev, stream=stream)
+        if dist_on:
+            dist.all_reduce(hist_dev)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device events; barrier + sync both sides) ----
+    clk_path = os.path.join(tempfile.gettempdir(), f"rkc_clocks_{rank}.csv")
+    sampler = clocks_sampler(clk_path, local_rank)
+    time.sleep(0.3)
+    pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+             for _ in range(args.steps)]
+    launches0 = rkc.rkc_launch_count()
+    if dist_on:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for i in range(args.steps):
+        one_step(pairs[i])
+    stop.record(stream)
+    torch.cuda.synchronize()
+    if dist_on:
+        dist.barrier()
+    launches = rkc.rkc_launch_count() - launches0
+    if sampler is not None:
+        sampler.terminate()
+        sampler.wait()
+    ms = start.elapsed_time(stop)
+    step_kernel_ms = sum(a.elapsed_time(b) for a, b in pairs)
+    t = torch.tensor([ms, step_kernel_ms], dtype=torch.float64, device=dev)
+    if dist_on:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, step_kernel_ms = float(t[0]), float(t[1])
+
+    # ---- e2e: the public C-ABI call with HOST buffers (pinned ops in, results out) ----
+    counters_host = np.zeros((TRACES, rkc.RKC_NCTR), dtype=np.uint32)
+    hist_host = np.zeros(rkc.RKC_NHIST, dtype=np.int64)
+    if dist_on:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        pool.rkc_pool_reset(stream)
+        _step_host(pool, ops_pinned, stream)
+        pool.rkc_telemetry_read(counters_out=counters_host, hist_out=hist_host, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
+    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if dist_on:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te[0])
+
+    # ---- telemetry of one replay for the algorithmic byte model (outside timing) ----
+    counters, events, hist = pool.read_all()
+    ab = algorithmic_bytes(ops, counters, events)
+    tot = torch.tensor([non_nop, TRACES], dtype=torch.float64, device=dev)
+    if dist_on:
+        dist.all_reduce(tot)
+    total_events, total_traces = float(tot[0]), float(tot[1])
+
+    clk = clocks_summary(clk_path)
+    if rank != 0:
+        if dist_on:
+            dist.destroy_process_group()
+        return
+    peak, peak_src = load_peak()
+    per_launch_ms = step_kernel_ms / (args.steps * TSTEPS)
+    achieved = ab["bytes"] / TSTEPS / (per_launch_ms * 1e-3) / 1e9
+    traffic = load_traffic()
+    value = total_events * args.steps / (ms * 1e-3)
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": workload_config(world),
+        "traces_per_s": total_traces * args.steps / (ms * 1e-3),
+        "events_per_step": total_events,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "rkc_step_kernel", "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": ab["bytes"] / TSTEPS,
+                     "avg_launch_us": per_launch_ms * 1e3,
+                     "step_kernel_share": step_kernel_ms / ms},
+        "e2e": {"value": total_events / (e2e_ms * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": int(ops_u8.size),
+                "d2h_bytes_per_step": int(counters_host.nbytes + hist_host.nbytes),
+                "ms_per_step": e2e_ms,
+                "path": "rkc_pool_reset + rkc_step_batch(pinned host ops) + "
+                        "rkc_telemetry_read(host counters + histogram)"},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfgs, ops)
+    print(json.dumps(out), flush=True)
+    if dist_on:
+        dist.destroy_process_group()
+
+
+def _step_host(pool, ops_pinned, stream):
+    # rkc_step_batch with a HOST (pinned) op stream: the library copies it in
+    # double-buffered chunks on its copy stream, overlapped with the steps
+    from paper_2605_24259_b200 import rkc
+    rkc._check(rkc._lib.rkc_step_batch(pool.handle, ops_pinned.data_ptr(), TSTEPS, 0,
+                                       stream.cuda_stream), "rkc_step_batch")
+
+
+if __name__ == "__main__":
+    main()
