@@ -231,6 +231,7 @@ rkc_status run_init(rkc_pool* p, cudaStream_t st) {
   init_blocks_kernel<<<grid_for((size_t)p->d.num_traces * p->d.NS), kThreads, 0, st>>>(p->d, p->tcfg);
   init_tables_kernel<<<grid_for(p->d.num_traces), kThreads, 0, st>>>(p->d, p->tcfg);
   CUDA_TRY(cudaMemsetAsync(p->staged, 0, sizeof(uint4) * p->d.num_traces, st));
+  CUDA_TRY(cudaMemsetAsync(p->d.bcnt, 0, 16 * 4, st));
   CUDA_TRY(cudaMemsetAsync(p->owner_tag, 0xFF, sizeof(uint32_t) * p->d.num_traces, st));
   CUDA_TRY(cudaGetLastError());
   p->step = 0;
@@ -356,6 +357,8 @@ rkc_status rkc_pool_create(const rkc_pool_config* config, const rkc_trace_config
   ALLOC(d.obj, T * d.O * 8);
   ALLOC(d.ctr, T * K_NCTR * 4);
   ALLOC(d.ev, T * (size_t)d.EPT * 32);
+  ALLOC(d.perm, T * 8 * 4);
+  ALLOC(d.bcnt, 16 * 4);
   ALLOC(p->tcfg, T * 12);
   ALLOC(p->staged, T * 16);
   ALLOC(p->owner_tag, T * 4);
