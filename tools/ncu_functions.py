@@ -16,9 +16,14 @@ def func_ranges(lib):
     cub = [f for f in glob.glob(os.path.join(d, "*.cubin")) if os.path.basename(f).startswith("rkc_step.")][0]
     out = subprocess.check_output(["readelf", "-sW", cub], text=True, stderr=subprocess.DEVNULL)
     rng = []
+    sect = None
     for line in out.splitlines():
         f = line.split()
-        if len(f) >= 8 and f[3] == "FUNC":
+        if len(f) >= 8 and f[3] == "FUNC" and f[-1].endswith("rkc_step_kernelENS_8StepArgsE"):
+            sect = f[-2]
+    for line in out.splitlines():
+        f = line.split()
+        if len(f) >= 8 and f[3] == "FUNC" and f[-2] == sect:
             off = int(f[1], 16)
             size = int(f[2], 16) if f[2].startswith("0x") else int(f[2])
             name = f[-1].split("$")[-1]
@@ -27,16 +32,19 @@ def func_ranges(lib):
     return sorted(rng)
 
 
-def main(rep, lib):
+def main(rep, lib, dump=None):
     out = subprocess.check_output(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                                   text=True)
     rows = list(csv.reader(out.splitlines()))
     hdr = rows[1]
     ai, ii, wi = hdr.index("Address"), hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
     data = []
+    src = {}
+    si = hdr.index("Source")
     for r in rows[2:]:
         try:
             data.append((int(r[ai], 16), int(r[ii]), int(r[wi])))
+            src[int(r[ai], 16)] = r[si].strip()
         except (ValueError, IndexError):
             break  # second kernel block starts
     base = data[0][0]
@@ -50,6 +58,8 @@ def main(rep, lib):
                 name = n
         inst[name] += i
         samp[name] += w
+        if dump and name == dump:
+            print(f"{off:6x} {i:10d} {w:6d} {src[(a)]}")
     ti, ts = sum(inst.values()), sum(samp.values())
     print(f"{'function':24s} {'inst':>12s} {'inst%':>6s} {'samples%':>8s}")
     for n, s in samp.most_common():
@@ -57,4 +67,4 @@ def main(rep, lib):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)
