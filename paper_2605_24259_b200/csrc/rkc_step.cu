@@ -267,9 +267,8 @@ __device__ __forceinline__ void fbm_set(uint32_t j, uint32_t nib) {
 
 // reclass pass: rewrite the class bits of every cached block whose owner is
 // marked, from the owner's bound claim; recount the protected blocks.
-__device__ __noinline__ void flush_reclass() {
-    if ((S.rc[0] | S.rc[1] | S.rc[2] | S.rc[3]) == 0) return;
-  prefetch_blocks(S.meta);
+__device__ __noinline__ void flush_reclass_pass() {
+    prefetch_blocks(S.meta);
   need_tables(true, true);
   const uint32_t low = lowering();
   for (uint32_t o = lane_id(); o < S.O; o += 32) {
@@ -327,6 +326,9 @@ __device__ __noinline__ void flush_reclass() {
   if (lane_id() < 4) S.rc[lane_id()] = 0;
   __syncwarp();
   refresh_protected();
+}
+__device__ __forceinline__ void flush_reclass() {
+  if (S.rc[0] | S.rc[1] | S.rc[2] | S.rc[3]) flush_reclass_pass();
 }
 
 // release request r's active blocks to FREE (deferral / refusal / no-admit)
@@ -1032,23 +1034,79 @@ __device__ __forceinline__ uint32_t bucket_of(uint32_t kind) {
   }
 }
 
-__global__ void __launch_bounds__(256) rkc_classify_kernel(const __grid_constant__ StepArgs args) {
+// K0: light pass, one thread per trace.  Completes the ops that provably
+// change nothing but a request record and a counter -- a NOP with no expiry
+// due, an ADVANCE that needs no new block (decode within the last block, or a
+// chunk that fits the blocks already held), an ADMIT whose PEAK check passes --
+// with the exact effects the warp path would have (no events, no block, claim,
+// object or header change).  Every other trace is bucketed by op kind for the
+// warp-per-trace step kernel, heavy block-scanning kinds first.
+__global__ void __launch_bounds__(256) rkc_light_kernel(const __grid_constant__ StepArgs args) {
   const PoolDev& p = args.p;
-  uint32_t* cnt = p.bcnt + (args.step & 1u) * 8;
-  if (blockIdx.x == 0 && threadIdx.x < 8) p.bcnt[((args.step + 1u) & 1u) * 8 + threadIdx.x] = 0;
+  const uint32_t step = args.step;
+  uint32_t* cnt = p.bcnt + (step & 1u) * 8;
+  if (blockIdx.x == 0 && threadIdx.x < 8) p.bcnt[((step + 1u) & 1u) * 8 + threadIdx.x] = 0;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t base = blockIdx.x * blockDim.x; base < p.num_traces; base += stride) {
     const uint32_t t = base + threadIdx.x;
     const bool valid = t < p.num_traces;
-    const uint32_t kind = valid ? (__ldcs(&args.ops[t].x) & 0xFFu) : 0u;
-    const uint32_t bk = valid ? bucket_of(kind) : 8u;
+    bool heavy = false;
+    uint32_t kind = 0;
+    if (valid) {
+      const uint4 opw = __ldcs(args.ops + t);
+      kind = opw.x & 0xFFu;
+      const uint32_t a = (opw.x >> 8) & 0xFFu;
+      const uint32_t* h = p.hdr + (size_t)t * H_NWORDS;
+      heavy = true;
+      if (kind == OP_NOP) {
+        heavy = step >= __ldcg(h + H_NEXT_EXPIRY);
+      } else if (kind == OP_ADVANCE && a < p.Q) {
+        uint32_t* rq = p.req + ((size_t)t * p.Q + a) * 8;
+        const uint4 r0 = __ldcg(reinterpret_cast<const uint4*>(rq));
+        const uint2 r1 = __ldcg(reinterpret_cast<const uint2*>(rq + 4));
+        const uint32_t nexp = __ldcg(h + H_NEXT_EXPIRY);
+        const uint32_t status = r0.x & 0xFFu, prompt = r0.y, chunk = r0.z, decode = r0.w;
+        const uint32_t done = r1.x, live = r1.y;
+        if (step < nexp && status == R_RUNNING && (uint64_t)done < (uint64_t)prompt + decode) {
+          const uint32_t n = done < prompt ? min(chunk, prompt - done) : 1u;
+          const uint64_t need_total = ((uint64_t)done + n + kBlockTokens - 1) / kBlockTokens;
+          if (need_total <= live) {
+            rq[RQ_DONE] = done + n;
+            atomicAdd(p.ctr + (size_t)t * K_NCTR + K_OPS, 1u);
+            heavy = false;
+          }
+        }
+      } else if (kind == OP_ADMIT && a < p.Q && ((opw.x >> 16) & 0xFFu) < p.O && (opw.x >> 24) <= 1 &&
+                 opw.y >= 1 && opw.z >= 1 && opw.y <= kMaxTokens && opw.w <= kMaxTokens) {
+        uint32_t* rq = p.req + ((size_t)t * p.Q + a) * 8;
+        const uint32_t status = __ldcg(rq) & 0xFFu;
+        const uint4 hv0 = __ldcg(reinterpret_cast<const uint4*>(h));       // U, policy, accept, seq
+        const uint4 hv1 = __ldcg(reinterpret_cast<const uint4*>(h) + 1);   // free, alive, P, mask
+        const uint32_t nexp = __ldcg(h + H_NEXT_EXPIRY);
+        if (step < nexp && status != R_RUNNING && status != R_DEFERRED) {
+          const uint64_t peak = ((uint64_t)opw.y + opw.w + kBlockTokens - 1) / kBlockTokens;
+          const bool peak_check = ((hv0.y >> 8) & 0xFFu) == ADMIT_PEAK;
+          if (!peak_check || (uint64_t)hv1.z + hv1.y + peak <= hv0.x) {
+            reinterpret_cast<uint4*>(rq)[0] =
+                make_uint4(R_RUNNING | ((opw.x >> 24) << 8) | (((opw.x >> 16) & 0xFFu) << 16), opw.y,
+                           opw.z, opw.w);
+            rq[RQ_DONE] = 0;
+            rq[RQ_LIVE] = 0;
+            atomicAdd(p.ctr + (size_t)t * K_NCTR + K_OPS, 1u);
+            atomicAdd(p.ctr + (size_t)t * K_NCTR + K_ADMITTED, 1u);
+            heavy = false;
+          }
+        }
+      }
+    }
+    const uint32_t bk = heavy ? bucket_of(kind) : 8u;
     const uint32_t grp = __match_any_sync(kFull, bk);
     const uint32_t leader = __ffs(grp) - 1;
     uint32_t off = 0;
-    if (lane == leader && valid) off = atomicAdd(cnt + bk, __popc(grp));
+    if (lane == leader && heavy) off = atomicAdd(cnt + bk, __popc(grp));
     off = __shfl_sync(kFull, off, leader);
-    if (valid) p.perm[(size_t)bk * p.num_traces + off + __popc(grp & lanemask_lt())] = t;
+    if (heavy) p.perm[(size_t)bk * p.num_traces + off + __popc(grp & lanemask_lt())] = t;
   }
 }
 
@@ -1058,7 +1116,9 @@ rkc_step_kernel(const __grid_constant__ StepArgs args) {
   // CTA i -> the i-th trace of the op-kind bucketed order of this step
   uint32_t t;
   {
-    const uint32_t* cnt = args.p.bcnt + (args.step & 1u) * 8;
+    const uint4* cnt4 = reinterpret_cast<const uint4*>(args.p.bcnt + (args.step & 1u) * 8);
+    const uint4 ca = __ldcg(cnt4), cb = __ldcg(cnt4 + 1);
+    const uint32_t cnt[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
     const uint32_t i = blockIdx.x;
     uint32_t acc = 0, bk = 8, off = 0;
 #pragma unroll
@@ -1098,6 +1158,9 @@ rkc_step_kernel(const __grid_constant__ StepArgs args) {
   if (kind == OP_COMPLETE || kind == OP_TOUCH) {  // these ops scan the block words
     const uint32_t* mb = p.meta + (size_t)t * p.NS;
     for (uint32_t l = lane; l < p.NS / 32; l += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(mb + l * 32));
+  } else if (kind == OP_ADVANCE || kind == OP_INSERT) {  // heavy ones allocate: keys next
+    const uint32_t* kb = p.key + (size_t)t * p.NS;
+    for (uint32_t l = lane; l < p.NS / 32; l += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(kb + l * 32));
   }
   const uint32_t next_exp = __shfl_sync(kFull, hw, H_NEXT_EXPIRY);
   // a NOP with no expiry due changes nothing (fast path)
@@ -1157,7 +1220,7 @@ cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, c
   g_launches += 1;
   StepArgs args{p, reinterpret_cast<const uint4*>(ops_step), step};
   const uint32_t cgrid = (p.num_traces + 255) / 256 < 148 * 8 ? (p.num_traces + 255) / 256 : 148 * 8;
-  rkc_classify_kernel<<<cgrid, 256, 0, st>>>(args);
+  rkc_light_kernel<<<cgrid, 256, 0, st>>>(args);
   rkc_step_kernel<<<p.num_traces, kWarpsPerCta * 32, 0, st>>>(args);
   return cudaGetLastError();
 }
