@@ -27,7 +27,8 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
-    cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), *SOURCES, "-o", LIB]
+    extra = os.environ.get("RKC_NVCC_EXTRA", "").split()
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), *SOURCES, "-o", LIB]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))

@@ -1075,6 +1075,52 @@ __global__ void __launch_bounds__(256) rkc_light_kernel(const __grid_constant__ 
             rq[RQ_DONE] = done + n;
             atomicAdd(p.ctr + (size_t)t * K_NCTR + K_OPS, 1u);
             heavy = false;
+          } else if (p.NS <= 1024) {
+            // a feasible allocation served entirely from free blocks: the
+            // `need` lowest-id free blocks get positions live.. (G24); no
+            // victim, no event, no claim or object change
+            const uint32_t need = (uint32_t)(need_total - live);
+            const uint4 hv0 = __ldcg(reinterpret_cast<const uint4*>(h));      // U, policy, accept, seq
+            const uint4 hv1 = __ldcg(reinterpret_cast<const uint4*>(h) + 1);  // free, alive, P, mask
+            if ((uint64_t)hv1.z + hv1.y + need <= hv0.x && need <= hv1.x) {
+              uint32_t* fbm = p.fbm + (size_t)t * (p.NS / 32);
+              uint32_t* key = p.key + (size_t)t * p.NS;
+              uint32_t* meta = p.meta + (size_t)t * p.NS;
+              const uint32_t nw4 = p.NS / 128;
+              uint4 fw[8];
+#pragma unroll
+              for (uint32_t q = 0; q < 8; ++q)
+                if (q < nw4) fw[q] = __ldcg(reinterpret_cast<const uint4*>(fbm) + q);
+              uint32_t taken = 0;
+#pragma unroll
+              for (uint32_t q = 0; q < 8; ++q) {
+                if (q >= nw4 || taken >= need) break;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  uint32_t word = el(fw[q], e);
+                  if (taken >= need || word == 0) continue;
+                  uint32_t tw = 0;
+                  while (word && taken < need) {
+                    const uint32_t bit = __ffs(word) - 1;
+                    word &= word - 1;
+                    tw |= 1u << bit;
+                    const uint32_t b = (q * 4 + e) * 32 + bit;
+                    meta[b] = meta_make(kResActive, a, live + taken);
+                    key[b] = kKeyActive;
+                    ++taken;
+                  }
+                  fbm[q * 4 + e] = el(fw[q], e) & ~tw;
+                }
+              }
+              uint32_t* hw = const_cast<uint32_t*>(h);
+              hw[H_FREE] = hv1.x - need;
+              hw[H_ALIVE] = hv1.y + need;
+              rq[RQ_LIVE] = live + need;
+              rq[RQ_DONE] = done + n;
+              atomicAdd(p.ctr + (size_t)t * K_NCTR + K_OPS, 1u);
+              atomicAdd(p.ctr + (size_t)t * K_NCTR + K_BLOCKS_ALLOCATED, need);
+              heavy = false;
+            }
           }
         }
       } else if (kind == OP_ADMIT && a < p.Q && ((opw.x >> 16) & 0xFFu) < p.O && (opw.x >> 24) <= 1 &&
