@@ -46,37 +46,58 @@ def workload_config(n_gpus: int) -> dict:
 # algorithmic bytes of the step kernel (DESIGN.md sec. 4 "byte model")
 # --------------------------------------------------------------------------
 def algorithmic_bytes(ops: np.ndarray, counters: np.ndarray, events: np.ndarray) -> dict:
-    """Bytes the method must move in this layout for one full replay.
+    """Bytes the method must move in this layout for one full replay, by what
+    each op semantically reads and writes:
 
-    per trace-step      : op 16 + hot header 64 (read)
-    per non-NOP op      : header write 64, claim table 32*C, object table 8*O (read)
-    per victim selection: selection keys 4*N + free bitmap N/8 (read),
-                          per taken block 12 (meta gather + meta/key write)
-    per free-only alloc : bitmap N/8, per block 8 (meta/key write)
-    per meta scan       : 4*N (COMPLETE, deferral/refusal release, TOUCH with L>0)
-    per event           : 32 (write)
+    every trace-step     : op 16 + hot header 64 (next expiry, U, P, Alive, free, policy)
+    ADMIT                : request 32 read + 32 write
+    ADVANCE              : request 32 read + 8 write (done, live)
+      free-only alloc    : free bitmap N/8 read + N/8 write + 8 per block (meta, key)
+      evicting alloc     : keys 4N + bitmap N/8 + claim table 32C + object table 8O
+                           (victim attribution) + 12 per taken block + header write 64
+    deferral / refusal   : meta scan 4N + 8 per released block + header write 64
+    COMPLETE             : request 32 + target object 8 + meta scan 4N + 8 per block + header 64
+    SUBMIT               : claim table 32C (duplicate, reserve rule) + object 8 + writes 40
+    DEMOTE / expiry      : claim 32 read + 32 write
+    claim-state change   : reclass pass meta 4N + keys 4N (accepted, demoted, expired, harmed)
+    INSERT               : object 8 + claim 32 + allocation as above + header write 64
+    TOUCH                : object 8 + claim 32 + meta scan 4N + key read+write 8 per leading block
+    event                : 32 (write); counters 4 per op (reduction)
     """
     T, n = ops.shape
-    non_nop = int((ops["kind"] != 0).sum())
-    kinds = events["type"]
-    vic = events[kinds == 12]
-    k_evict = int(vic["f"][:, 3].astype(np.int64).sum())
+    kind = ops["kind"]
+    N = NBLK
+    et = events["type"]
+    cnt = {k: int((kind == k).sum()) for k in range(8)}
+    non_nop = n * T - cnt[0]
+    vic = events[et == 12]
     n_evict = len(vic)
-    blocks_alloc = int(counters[:, 21].astype(np.int64).sum())
-    k_free = blocks_alloc - k_evict
-    adv_ins = int(((ops["kind"] == 3) | (ops["kind"] == 5)).sum())
-    served = int((kinds == 11).sum())
-    released = int(((kinds == 7) | (kinds == 8)).sum())
-    touch_scan = int(((kinds == 13) & (events["f"][:, 1] > 0)).sum())
-    n_events = len(events)
+    k_evict = int(vic["f"][:, 3].astype(np.int64).sum())
+    k_all = int(counters[:, 21].astype(np.int64).sum())
+    k_free = max(0, k_all - k_evict)
+    n_alloc_free = int((counters[:, 21] > 0).sum())  # lower bound on free-only allocations
+    refusals = int(((et == 7) | (et == 8)).sum())
+    served = int((et == 11).sum())
+    served_blocks = int(events[et == 11]["f"][:, 1].astype(np.int64).sum())
+    probes = events[et == 13]
+    touch_scans = int((probes["f"][:, 1] > 0).sum())
+    touch_blocks = int(probes["f"][:, 1].astype(np.int64).sum())
+    claim_changes = int(((et == 1) | (et == 4) | (et == 5) | (et == 6)).sum())
     b = 0
-    b += T * n * (16 + 64)
-    b += non_nop * (64 + 32 * C + 8 * O)
-    b += n_evict * (4 * NBLK + NBLK // 8) + 12 * k_evict
-    b += max(0, adv_ins - n_evict) * (NBLK // 8) + 8 * max(0, k_free)
-    b += (served + released + touch_scan) * 4 * NBLK
-    b += 32 * n_events
-    return dict(bytes=int(b), non_nop=non_nop, evicting_selections=n_evict, events=n_events)
+    b += n * T * (16 + 64)
+    b += cnt[2] * 64
+    b += cnt[3] * 40
+    b += k_free * 8 + n_alloc_free * (N // 4)
+    b += n_evict * (4 * N + N // 8 + 32 * C + 8 * O + 64) + 12 * k_evict
+    b += refusals * (4 * N + 64)
+    b += served * (32 + 8 + 4 * N + 64) + 8 * served_blocks
+    b += cnt[1] * (32 * C + 8 + 40)
+    b += (cnt[6] + int((et == 5).sum())) * 64
+    b += claim_changes * 8 * N
+    b += cnt[5] * (8 + 32 + 64)
+    b += touch_scans * 4 * N + cnt[7] * 40 + 8 * touch_blocks
+    b += 32 * len(events) + 4 * non_nop
+    return dict(bytes=int(b), non_nop=non_nop, evicting_selections=n_evict, events=len(events))
 
 
 # --------------------------------------------------------------------------

@@ -52,7 +52,7 @@ struct alignas(16) Warp {      // the warp's shared memory (one warp per CTA)
   alignas(16) uint32_t cl[32][8];  // claim records (lane c owns claim c)
   uint32_t obj0[128];          // object word 0
   uint32_t lead[128];          // leading prefix per object
-  alignas(16) union {
+  union alignas(16) {
     struct { uint32_t lim3[128], lim2[128], cnt3[128]; };  // reclass scratch
     uint32_t keys[kStageMax];  // staged selection keys (alloc only)
   };
