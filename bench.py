@@ -29,17 +29,33 @@ sys.path.insert(0, ROOT)
 
 METRIC = "allocator events/sec and traces/sec at 1/2/4/8 B200; % of HBM roofline"
 UNIT = "events/s"
-TRACES, NBLK, TSTEPS, C, Q, O = 100_000, 1024, 256, 16, 16, 64
-EPT = 512
 SEED = 0
+# workloads: c3 is the bench default (BASELINE.json configs[2]);
+# c4 (configs[3]) is selectable with --config c4
+WORKLOADS = {
+    "c3": dict(recipe=3, traces=100_000, nblk=1024, steps=256, C=16, Q=16, O=64, ept=512,
+               desc="c3: 100k random traces per GPU, 1024-block pools (16-token blocks), T=256 "
+                    "lockstep steps, mixed chunked prefill/decode, 4-16 claims",
+               l2="inputs larger than L2: pool state 0.83 GB + ops 0.41 GB per GPU, no flush"),
+    "c4": dict(recipe=4, traces=10_000, nblk=65536, steps=1024, C=16, Q=16, O=128, ept=1024,
+               desc="c4: 10k random traces per GPU, 65536-block pools (Llama-3-8B-sized KV), "
+                    "T=1024 lockstep steps, long shared prefixes, demotion/expiry churn",
+               l2="inputs larger than L2: pool state 5.2 GB + ops 0.16 GB per GPU, no flush"),
+}
+WL = WORKLOADS["c3"]
+TRACES, NBLK, TSTEPS, C, Q, O, EPT = (WL[k] for k in ("traces", "nblk", "steps", "C", "Q", "O", "ept"))
+
+
+def select_workload(name: str):
+    global WL, TRACES, NBLK, TSTEPS, C, Q, O, EPT
+    WL = WORKLOADS[name]
+    TRACES, NBLK, TSTEPS, C, Q, O, EPT = (WL[k] for k in ("traces", "nblk", "steps", "C", "Q", "O", "ept"))
 
 
 def workload_config(n_gpus: int) -> dict:
-    return {"workload": "c3: 100k random traces per GPU, 1024-block pools (16-token blocks), "
-                        "T=256 lockstep steps, mixed chunked prefill/decode, 4-16 claims",
-            "traces_per_gpu": TRACES, "pool_blocks": NBLK, "steps_per_replay": TSTEPS,
-            "global_traces": TRACES * n_gpus, "parallelism": f"trace-sharded x{n_gpus}",
-            "l2": "inputs larger than L2: pool state 0.83 GB + ops 0.41 GB per GPU, no flush"}
+    return {"workload": WL["desc"], "traces_per_gpu": TRACES, "pool_blocks": NBLK,
+            "steps_per_replay": TSTEPS, "global_traces": TRACES * n_gpus,
+            "parallelism": f"trace-sharded x{n_gpus}", "l2": WL["l2"]}
 
 
 # --------------------------------------------------------------------------
@@ -160,7 +176,7 @@ def cpu_baseline(cfgs, ops, budget_s: float = 12.0) -> dict:
     same workload (the first traces of rank 0's shard)."""
     from oracle import oracle as orc
     nthreads = os.cpu_count() or 1
-    chunk = max(64, 16 * nthreads)
+    chunk = max(64, 16 * nthreads) if WL["recipe"] == 3 else max(4, nthreads)
     done_traces, ops_done, t_used = 0, 0, 0.0
     while t_used < budget_s and done_traces < ops.shape[1]:
         sl = slice(done_traces, min(done_traces + chunk, ops.shape[1]))
@@ -172,7 +188,7 @@ def cpu_baseline(cfgs, ops, budget_s: float = 12.0) -> dict:
         ops_done += int((sub["kind"] != 0).sum())
         done_traces = sl.stop
     return {"value": ops_done / t_used, "unit": UNIT, "cores": nthreads, "kind": "oracle",
-            "sample": f"first {done_traces} traces of the c3 workload x {TSTEPS} steps "
+            "sample": f"first {done_traces} traces of the {WL['desc'][:2]} workload x {TSTEPS} steps "
                       f"({ops_done} non-NOP ops) in {t_used:.1f} s, plain C++ oracle (-O2), "
                       f"{nthreads} threads, one trace per task",
             "traces_per_s": done_traces / t_used}
@@ -185,8 +201,8 @@ def run_reference(args, rank: int, world: int):
     from paper_2605_24259_b200 import gen
     from oracle import oracle as orc
     nthreads = os.cpu_count() or 1
-    sample = max(64, 32 * nthreads)
-    cfgs, ops = gen.random_traces(3, SEED, 0, sample, TSTEPS, NBLK, C, Q, O)
+    sample = max(64, 32 * nthreads) if WL["recipe"] == 3 else max(8, nthreads)
+    cfgs, ops = gen.random_traces(WL["recipe"], SEED, 0, sample, TSTEPS, NBLK, C, Q, O)
     non_nop = int((ops["kind"] != 0).sum())
     times = []
     for i in range(args.warmup + args.steps):
@@ -198,7 +214,7 @@ def run_reference(args, rank: int, world: int):
             times.append(dt)
     t = float(np.sum(times))
     value = non_nop * args.steps / t
-    desc = (f"each step: the first {sample} traces of the c3 workload x {TSTEPS} steps "
+    desc = (f"each step: the first {sample} traces of the {WL['desc'][:2]} workload x {TSTEPS} steps "
             f"({non_nop} non-NOP ops), plain C++ oracle, {nthreads} threads")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -221,7 +237,9 @@ def main():
     ap.add_argument("--impl", default="rkc", choices=["rkc", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default="c3", choices=sorted(WORKLOADS))
     args = ap.parse_args()
+    select_workload(args.config)
     args.warmup = max(3, args.warmup)
 
     rank = int(os.environ.get("RANK", "0"))
@@ -243,7 +261,7 @@ def main():
     dev = torch.device("cuda", local_rank)
 
     # ---- inputs: this rank's shard, generated on the host, resident in HBM ----
-    cfgs, ops = gen.random_traces(3, SEED, rank * TRACES, TRACES, TSTEPS, NBLK, C, Q, O)
+    cfgs, ops = gen.random_traces(WL["recipe"], SEED, rank * TRACES, TRACES, TSTEPS, NBLK, C, Q, O)
     non_nop = int((ops["kind"] != 0).sum())
     ops_u8 = ops.view(np.uint8).reshape(-1)
     ops_dev = torch.from_numpy(ops_u8).to(dev)
