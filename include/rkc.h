@@ -246,6 +246,36 @@ RKC_API rkc_status rkc_state_import(rkc_pool* pool, uint32_t trace_begin, uint32
                             const rkc_claim_view* claims, const rkc_request_view* requests,
                             const rkc_object_view* objects);
 
+/* ---- conformance ---------------------------
+ * Per-trace replay of the claim-level event stream reconstructing every
+ * claim's lifecycle.  verdict bit set = check FAILED for that trace. */
+#define RKC_CHECK_L1 0x01u   /* harm only after acceptance + materialization      */
+#define RKC_CHECK_L2 0x02u   /* write-admission denial followed by service        */
+#define RKC_CHECK_L3 0x04u   /* refusal capacity proof and blocking attribution   */
+#define RKC_CHECK_L45 0x08u  /* release (demote / expire) before loss, no harm    */
+#define RKC_CHECK_L6 0x10u   /* materialization predicate consistency             */
+#define RKC_CHECK_L7 0x20u   /* lifecycle legality / reconstruction = final state */
+#define RKC_CHECK_I4 0x40u   /* contract lowering never harms an obligated claim  */
+#define RKC_CHECK_LOST 0x80u /* the trace's event ring overflowed                 */
+/* evidence int64[RKC_NEVIDENCE]: accepted, materialized, harmed, refusals
+ * (incl. deferrals and insert refusals), attributed refusals, victims,
+ * after-release victims, write-admission denials, failing traces */
+#define RKC_NEVIDENCE 9
+/* Check a compacted event stream (device pointers): events in (trace, step,
+ * seq) order, offsets [num_traces+1] exclusive prefix, optional final claim
+ * states [num_traces][claims_per_trace] (u8) and lowering bytes [num_traces].
+ * verdict_out [num_traces] u32 and evidence_out int64[RKC_NEVIDENCE] are
+ * device pointers (evidence is accumulated: zero it first). */
+RKC_API rkc_status rkc_conformance_check(const rkc_event* events, const uint32_t* offsets,
+                                         uint32_t num_traces, const uint8_t* final_claim_states,
+                                         uint32_t claims_per_trace, const uint8_t* lowering,
+                                         uint32_t* verdict_out, int64_t* evidence_out, void* stream);
+/* Check a pool's own event rings against its final claim table (device
+ * outputs; a trace whose ring overflowed or was drained reports LOST /
+ * skips the final-state comparison). */
+RKC_API rkc_status rkc_pool_conformance(rkc_pool* pool, uint32_t* verdict_out, int64_t* evidence_out,
+                                        void* stream);
+
 /* Number of staged ops dropped because another op for the same trace was
  * already staged in this step (device-side staging conflicts). */
 RKC_API rkc_status rkc_staging_conflicts(rkc_pool* pool, uint64_t* out);

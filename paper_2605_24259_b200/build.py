@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = [os.path.join(CSRC, f) for f in ("rkc_step.cu", "rkc_abi.cu")]
+SOURCES = [os.path.join(CSRC, f) for f in ("rkc_step.cu", "rkc_abi.cu", "rkc_conformance.cu")]
 HEADERS = [os.path.join(CSRC, "rkc_internal.cuh"), os.path.join(ROOT, "include", "rkc.h")]
 LIB = os.path.join(HERE, "librkc.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

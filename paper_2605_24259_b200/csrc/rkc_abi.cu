@@ -15,6 +15,11 @@
 namespace rkc {
 cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, cudaStream_t st);
 std::atomic<unsigned long long> g_launches{0};  // kernels this library launched
+cudaError_t launch_conformance_array(const void* events, const uint32_t* offsets, uint32_t T,
+                                     const uint8_t* final_states, uint32_t C, const uint8_t* lowering,
+                                     uint32_t* verdict, unsigned long long* evidence, cudaStream_t st);
+cudaError_t launch_conformance_pool(const PoolDev& p, uint32_t* verdict, unsigned long long* evidence,
+                                    cudaStream_t st);
 }
 
 using namespace rkc;
@@ -728,6 +733,29 @@ rkc_status rkc_state_import(rkc_pool* pool, uint32_t trace_begin, uint32_t n,
 }
 
 unsigned long long rkc_launch_count(void) { return g_launches.load(); }
+
+rkc_status rkc_conformance_check(const rkc_event* events, const uint32_t* offsets,
+                                 uint32_t num_traces, const uint8_t* final_claim_states,
+                                 uint32_t claims_per_trace, const uint8_t* lowering,
+                                 uint32_t* verdict_out, int64_t* evidence_out, void* stream) {
+  if (!offsets || !verdict_out || claims_per_trace > 32 || (num_traces && !events && false))
+    return RKC_E_INVAL;
+  if (num_traces == 0) return RKC_OK;
+  CUDA_TRY(launch_conformance_array(events, offsets, num_traces, final_claim_states,
+                                    claims_per_trace, lowering, verdict_out,
+                                    reinterpret_cast<unsigned long long*>(evidence_out),
+                                    (cudaStream_t)stream));
+  return RKC_OK;
+}
+
+rkc_status rkc_pool_conformance(rkc_pool* pool, uint32_t* verdict_out, int64_t* evidence_out,
+                                void* stream) {
+  if (!pool || !verdict_out) return RKC_E_INVAL;
+  CUDA_TRY(launch_conformance_pool(pool->d, verdict_out,
+                                   reinterpret_cast<unsigned long long*>(evidence_out),
+                                   (cudaStream_t)stream));
+  return RKC_OK;
+}
 
 // the pool step counter can be set for injected states (test-only)
 rkc_status rkc_state_set_step(rkc_pool* pool, uint64_t step) {

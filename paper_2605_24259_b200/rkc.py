@@ -85,6 +85,8 @@ _sigs = {
     "rkc_staging_conflicts": (ctypes.c_int32, [_vp, ctypes.POINTER(_u64)]),
     "rkc_state_set_step": (ctypes.c_int32, [_vp, _u64]),
     "rkc_launch_count": (ctypes.c_ulonglong, []),
+    "rkc_conformance_check": (ctypes.c_int32, [_vp, _vp, _u32, _vp, _u32, _vp, _vp, _vp, _vp]),
+    "rkc_pool_conformance": (ctypes.c_int32, [_vp, _vp, _vp, _vp]),
 }
 for _name, (_res, _args) in _sigs.items():
     _f = getattr(_lib, _name)
@@ -92,6 +94,13 @@ for _name, (_res, _args) in _sigs.items():
     _f.argtypes = _args
 
 EXPORTED_SYMBOLS = tuple(_sigs)
+
+
+RKC_CHECK = {"L1": 0x01, "L2": 0x02, "L3": 0x04, "L45": 0x08, "L6": 0x10, "L7": 0x20, "I4": 0x40,
+             "LOST": 0x80}
+RKC_NEVIDENCE = 9
+EVIDENCE_NAMES = ["accepted", "materialized", "harmed", "refusals", "attributed_refusals", "victims",
+                  "after_release_victims", "write_denials", "failing_traces"]
 
 
 class RkcError(RuntimeError):
@@ -286,8 +295,33 @@ class Pool:
         _check(_lib.rkc_state_import(self.handle, trace_begin, n, *[a.ctypes.data for a in arrs]),
                "rkc_state_import")
 
+    def rkc_pool_conformance(self, stream=None):
+        """Conformance L1-L7 over this pool's event rings; returns (verdict, evidence)
+        device tensors."""
+        import torch
+        verdict = torch.zeros(self.num_traces, dtype=torch.int32, device=f"cuda:{self.device}")
+        evidence = torch.zeros(RKC_NEVIDENCE, dtype=torch.int64, device=f"cuda:{self.device}")
+        _check(_lib.rkc_pool_conformance(self.handle, _ptr(verdict), _ptr(evidence), _stream(stream)),
+               "rkc_pool_conformance")
+        return verdict, evidence
+
     def rkc_state_set_step(self, step: int):
         _check(_lib.rkc_state_set_step(self.handle, step), "rkc_state_set_step")
+
+
+def rkc_conformance_check(events_dev, offsets_dev, num_traces: int, final_states_dev=None,
+                          claims_per_trace: int = 16, lowering_dev=None, stream=None):
+    """Conformance L1-L7 over a compacted device event stream; returns
+    (verdict[num_traces] u32 tensor, evidence int64[RKC_NEVIDENCE] tensor)."""
+    import torch
+    dev = events_dev.device
+    verdict = torch.zeros(num_traces, dtype=torch.int32, device=dev)
+    evidence = torch.zeros(RKC_NEVIDENCE, dtype=torch.int64, device=dev)
+    _check(_lib.rkc_conformance_check(_ptr(events_dev), _ptr(offsets_dev), num_traces,
+                                      _ptr(final_states_dev), claims_per_trace, _ptr(lowering_dev),
+                                      _ptr(verdict), _ptr(evidence), _stream(stream)),
+           "rkc_conformance_check")
+    return verdict, evidence
 
 
 def rkc_pool_create(trace_cfgs, max_blocks, **kw) -> Pool:
