@@ -11,5 +11,5 @@ fi
 timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
 NCU=/usr/local/cuda/bin/ncu
 timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv python tools/profile_run.py > $OUT/launches.log 2>&1; echo "ncu list rc=$?" >> $OUT/launches.log
-timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"rkc_(step|light)_kernel" -s 256 -c 2 -o $OUT/prof_step python tools/profile_run.py > $OUT/prof.log 2>&1; echo "ncu full rc=$?" >> $OUT/prof.log
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"rkc_(step|light|evict)_kernel" -s 384 -c 3 -o $OUT/prof_step python tools/profile_run.py > $OUT/prof.log 2>&1; echo "ncu full rc=$?" >> $OUT/prof.log
 ls -la $OUT
