@@ -123,7 +123,7 @@ def clocks_sampler(path: str, gpu_index: int):
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
     try:
         return subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={q}",
-                                 "--format=csv,noheader,nounits", "-lms", "200"],
+                                 "--format=csv,noheader,nounits", "-lms", "100"],
                                 stdout=open(path, "w"), stderr=subprocess.DEVNULL)
     except Exception:
         return None
@@ -232,7 +232,7 @@ def run_reference(args, rank: int, world: int):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="rkc", choices=["rkc", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -254,11 +254,20 @@ def main():
     build.build()
     from paper_2605_24259_b200 import rkc
 
-    torch.cuda.set_device(local_rank)
+    # one process per GPU; RKC_BENCH_SAME_GPU=1 + RKC_DIST_BACKEND=gloo lets the
+    # multi-rank path be exercised with several ranks on one device (testing only)
+    ndev = torch.cuda.device_count()
+    gpu = local_rank if not os.environ.get("RKC_BENCH_SAME_GPU") else local_rank % max(1, ndev)
+    torch.cuda.set_device(gpu)
     dist_on = world > 1
     if dist_on:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    dev = torch.device("cuda", local_rank)
+        backend = os.environ.get("RKC_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group(backend)
+    dev = torch.device("cuda", gpu)
+    local_rank = gpu
 
     # ---- inputs: this rank's shard, generated on the host, resident in HBM ----
     cfgs, ops = gen.random_traces(WL["recipe"], SEED, rank * TRACES, TRACES, TSTEPS, NBLK, C, Q, O)
