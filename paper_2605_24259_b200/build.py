@@ -8,8 +8,10 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = [os.path.join(CSRC, f) for f in ("rkc_step.cu", "rkc_abi.cu", "rkc_conformance.cu")]
-HEADERS = [os.path.join(CSRC, "rkc_internal.cuh"), os.path.join(ROOT, "include", "rkc.h")]
+SOURCES = [os.path.join(CSRC, f) for f in ("rkc_step_o64.cu", "rkc_step_o128.cu", "rkc_abi.cu",
+                                           "rkc_conformance.cu")]
+HEADERS = [os.path.join(CSRC, f) for f in ("rkc_internal.cuh", "rkc_step_impl.cuh")] + \
+    [os.path.join(ROOT, "include", "rkc.h")]
 LIB = os.path.join(HERE, "librkc.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -24,16 +26,19 @@ def stale() -> bool:
     return any(os.path.getmtime(f) > t for f in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: tuple[str, ...] = ()) -> str:
+    """Compile librkc.so; `out` / `defines` build an experiment variant beside it."""
+    lib = out or LIB
+    if not force and out is None and not stale():
         return LIB
-    extra = os.environ.get("RKC_NVCC_EXTRA", "").split()
-    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), *SOURCES, "-o", LIB]
+    extra = os.environ.get("RKC_NVCC_EXTRA", "").split() + [f"-D{d}" for d in defines]
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), *SOURCES, "-o", lib]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))
     subprocess.check_call(cmd)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -13,8 +13,19 @@
 #include "rkc_internal.cuh"
 
 namespace rkc {
+namespace o64 {
 cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, cudaStream_t st);
+}
+namespace o128 {
+cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, cudaStream_t st);
+}
 std::atomic<unsigned long long> g_launches{0};  // kernels this library launched
+
+// one lockstep step = light pass + step kernel, from the build sized for the pool's object table
+static cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, cudaStream_t st) {
+  g_launches += 2;
+  return p.O <= 64 ? o64::launch_step(p, ops_step, step, st) : o128::launch_step(p, ops_step, step, st);
+}
 cudaError_t launch_conformance_array(const void* events, const uint32_t* offsets, uint32_t T,
                                      const uint8_t* final_states, uint32_t C, const uint8_t* lowering,
                                      uint32_t* verdict, unsigned long long* evidence, cudaStream_t st);

@@ -1,4 +1,4 @@
-// rkc_step.cu -- K1: the lockstep step kernel.
+// rkc_step_impl.cuh -- K0 light pass + K1 lockstep step kernel.
 //
 // One warp owns one trace (one paged KV pool) for one step:
 //   a0 op fetch -> a1 expiry -> a2 claim decision | a3 feasibility (P + A <= U,
@@ -16,18 +16,31 @@
 // words are streamed with coalesced 16-byte loads, lane L of vector j owning
 // blocks (j*32 + L)*4 .. +3; the selection keys of a <= 1024-block pool are
 // staged once in shared memory for the threshold search.
+#pragma once
 #include <cuda_runtime.h>
 
-#include <atomic>
 #include <cstddef>
 
 #include "rkc_internal.cuh"
 
 namespace rkc {
+namespace RKC_STEP_NS {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
-constexpr int kWarpsPerCta = 1;
+#ifndef RKC_WARPS_PER_CTA
+#define RKC_WARPS_PER_CTA 1
+#endif
+// independent warps per CTA, each its own trace (1 measured best: a CTA of
+// several warps holds its slot until its slowest trace is done)
+constexpr int kWarpsPerCta = RKC_WARPS_PER_CTA;
 constexpr uint32_t kStageMax = 1024;  // pools up to this size stage keys in smem
+// Object slots held in shared memory.  This file is compiled twice
+// (rkc_step_o64.cu / rkc_step_o128.cu): pools with O <= 64 run the 64-slot
+// build, whose 6 KB warp state fits 32 resident CTAs per SM instead of 30.
+#ifndef RKC_OMAX
+#error "compile through rkc_step_o64.cu / rkc_step_o128.cu"
+#endif
+constexpr uint32_t kObjMax = RKC_OMAX;
 
 enum : uint32_t { F_CLAIMS = 1, F_OBJS = 2, F_POST = 4, F_CLAIMS_CHANGED = 8, F_HDR = 16, F_RQ = 32 };
 
@@ -50,8 +63,8 @@ struct alignas(16) Warp {      // the warp's shared memory (one warp per CTA)
   uint32_t objdirty[4];
   uint32_t ctr[32];            // counter deltas of this step
   alignas(16) uint32_t cl[32][8];  // claim records (lane c owns claim c)
-  uint32_t obj0[128];          // object word 0
-  uint32_t lead[128];          // leading prefix per object
+  uint32_t obj0[kObjMax];      // object word 0
+  uint32_t lead[kObjMax];      // leading prefix per object
   union alignas(16) {
     struct { uint32_t lim3[128], lim2[128], cnt3[128]; };  // reclass scratch
     uint32_t keys[kStageMax];  // staged selection keys (alloc only)
@@ -60,7 +73,8 @@ struct alignas(16) Warp {      // the warp's shared memory (one warp per CTA)
 
 static_assert(offsetof(Warp, cl) % 16 == 0, "uint4 access to claim rows");
 static_assert(offsetof(Warp, keys) % 16 == 0, "uint4 access to staged keys");
-__shared__ Warp S;
+__shared__ Warp S_[kWarpsPerCta];
+#define S (S_[kWarpsPerCta == 1 ? 0u : (threadIdx.x >> 5)])
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
@@ -172,7 +186,7 @@ __device__ __forceinline__ void need_tables(bool claims, bool objs) {
   if (!claims && !objs) return;
   const uint32_t lane = lane_id();
   uint4 c0 = make_uint4(0, 0, 0, 0), c1 = make_uint4(0, 0, 0, 0);
-  uint2 ov[4];
+  uint2 ov[4] = {make_uint2(0, 0), make_uint2(0, 0), make_uint2(0, 0), make_uint2(0, 0)};
   if (claims && lane < S.C) {
     const uint4* cp = reinterpret_cast<const uint4*>(S.clm + lane * 8);
     c0 = __ldcg(cp);
@@ -202,6 +216,7 @@ __device__ __forceinline__ void need_tables(bool claims, bool objs) {
 }
 __device__ __noinline__ void need_claims() { need_tables(true, false); }
 __device__ __noinline__ void need_objs() { need_tables(false, true); }
+__device__ __noinline__ void need_both() { need_tables(true, true); }
 // pull one trace's block array into L2 ahead of a scan (one 128-B line per lane-iteration)
 __device__ __forceinline__ void prefetch_blocks(const uint32_t* base) {
   for (uint32_t l = lane_id(); l < S.NS / 32; l += 32)
@@ -269,7 +284,7 @@ __device__ __forceinline__ void fbm_set(uint32_t j, uint32_t nib) {
 // marked, from the owner's bound claim; recount the protected blocks.
 __device__ __noinline__ void flush_reclass_pass() {
     prefetch_blocks(S.meta);
-  need_tables(true, true);
+  need_both();
   const uint32_t low = lowering();
   for (uint32_t o = lane_id(); o < S.O; o += 32) {
     uint32_t l3 = 0, l2 = 0;
@@ -288,6 +303,7 @@ __device__ __noinline__ void flush_reclass_pass() {
   const uint4* meta4 = reinterpret_cast<const uint4*>(S.meta);
   const uint4* key4 = reinterpret_cast<const uint4*>(key);
   const uint32_t nv = S.nv;
+#pragma unroll 1
   for (uint32_t j = 0; j < nv; ++j) {
     const uint4 mv = __ldcg(meta4 + j * 32 + lane_id());
     bool any = false;
@@ -339,6 +355,7 @@ __device__ __noinline__ void release_blocks(uint32_t r) {
   const uint4* meta4 = reinterpret_cast<const uint4*>(meta);
   uint32_t freed = 0;
   const uint32_t nv = S.nv;
+#pragma unroll 1
   for (uint32_t j = 0; j < nv; ++j) {
     const uint4 mv = __ldcg(meta4 + j * 32 + lane_id());
     uint32_t nib = 0;
@@ -442,11 +459,27 @@ template <bool staged>
 __device__ __noinline__ uint32_t count_le(uint32_t T) {
   uint32_t c = 0;
   const uint32_t nv = S.nv;
+#pragma unroll 1
   for (uint32_t j = 0; j < nv; ++j) {
     const uint4 v = key_vec(j, staged);
     c += (v.x <= T) + (v.y <= T) + (v.z <= T) + (v.w <= T);
   }
   return __reduce_add_sync(kFull, c);
+}
+
+// smallest class-2 (soft) key: d2 = key - 2^31 maps class 2 to [0, 2^30) below
+// every other class (rare path: class 1 cannot cover the shortfall)
+template <bool staged>
+__device__ __noinline__ uint32_t min_class2() {
+  constexpr uint32_t kC2 = 2u << kClassShift;
+  uint32_t m2 = kFull;
+  const uint32_t nv = S.nv;
+#pragma unroll 1
+  for (uint32_t j = 0; j < nv; ++j) {
+    const uint4 v = key_vec(j, staged);
+    m2 = min(min(m2, v.x - kC2), min(v.y - kC2, min(v.z - kC2, v.w - kC2)));
+  }
+  return __reduce_min_sync(kFull, m2) + kC2;
 }
 
 // Free-only allocation (k <= free count): the k lowest-id free blocks, lane =
@@ -512,15 +545,18 @@ __device__ __noinline__ void alloc_evict(uint32_t k, uint32_t owner, bool insert
   const uint32_t nv = S.nv;
   const uint32_t lane = lane_id();
   const uint4* key4 = reinterpret_cast<const uint4*>(S.key);
-  uint32_t c1 = 0, mn1 = kFull, mn2 = kFull;
+  // one stats pass: d = key - 2^30 maps class 1 to [0, 2^30) and every free
+  // key above all others, so min(d) is the smallest non-free key and
+  // #{d < 2^30} the class-1 count (the class-2 minimum is needed only when
+  // class 1 cannot cover the shortfall: a second pass then)
+  constexpr uint32_t kC1 = 1u << kClassShift;
+  uint32_t c1 = 0, md = kFull;
   auto stat = [&](const uint4& v) {
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const uint32_t kk = el(v, e);
-      const uint32_t cls = kk >> kClassShift;
-      c1 += cls == 1 ? 1u : 0u;
-      mn1 = cls == 1 ? min(mn1, kk) : mn1;
-      mn2 = cls == 2 ? min(mn2, kk) : mn2;
+      const uint32_t d = el(v, e) - kC1;
+      c1 += d < kC1 ? 1u : 0u;
+      md = min(md, d);
     }
   };
   if (staged) {
@@ -539,13 +575,16 @@ __device__ __noinline__ void alloc_evict(uint32_t k, uint32_t owner, bool insert
     }
     __syncwarp();
   } else {
-    need_tables(true, true);
+    need_both();
     for (uint32_t j = 0; j < nv; ++j) stat(__ldcg(key4 + j * 32 + lane));
   }
   c1 = __reduce_add_sync(kFull, c1);
   uint32_t lo, clo, top;
-  if (k - fr <= c1) { lo = __reduce_min_sync(kFull, mn1) - 1; clo = fr; top = (2u << kClassShift) - 1; }
-  else { lo = __reduce_min_sync(kFull, mn2) - 1; clo = fr + c1; top = (3u << kClassShift) - 1; }
+  if (k - fr <= c1) {
+    lo = __reduce_min_sync(kFull, md) + kC1 - 1; clo = fr; top = (2u << kClassShift) - 1;
+  } else {  // the soft class is reached: smallest class-2 key
+    lo = min_class2<staged>() - 1; clo = fr + c1; top = (3u << kClassShift) - 1;
+  }
   uint32_t hi = top, chi = 0;
   bool bracket = false;
   uint32_t mult = 1;
@@ -588,6 +627,7 @@ __device__ __noinline__ void alloc_evict(uint32_t k, uint32_t owner, bool insert
   uint32_t ord = 0, rel = 0, clm = 0;
   uint32_t listed = 0, done_pos = 0;
   auto drain = [&](uint32_t n) {
+#pragma unroll 1
     for (uint32_t i = lane_id(); i < n; i += 32) {
       const uint32_t e = list[i];
       const uint32_t bb = e & 0x7FFFFFFFu;
@@ -616,6 +656,7 @@ __device__ __noinline__ void alloc_evict(uint32_t k, uint32_t owner, bool insert
     __syncwarp();
     done_pos += n;
   };
+#pragma unroll 1
   for (uint32_t j = 0; j < nv && done_pos + listed < k; ++j) {
     const uint4 v = key_vec(j, staged);
     const uint32_t tb = (v.x <= T ? 1u : 0u) | (v.y <= T ? 2u : 0u) | (v.z <= T ? 4u : 0u) |
@@ -659,7 +700,7 @@ __device__ __noinline__ void alloc_evict(uint32_t k, uint32_t owner, bool insert
 __device__ __noinline__ void alloc(uint32_t k, uint32_t owner, bool insert,
                                    uint32_t base) {
   flush_reclass();
-  if (insert) need_tables(true, true);
+  if (insert) need_both();
   if (k <= S.h[H_FREE]) alloc_free(k, owner, insert, base);
   else if (S.NS <= kStageMax) alloc_evict<true>(k, owner, insert, base);
   else alloc_evict<false>(k, owner, insert, base);
@@ -804,6 +845,7 @@ __device__ __noinline__ void op_complete(const Op op) {
     const uint4* meta4 = reinterpret_cast<const uint4*>(meta);
     uint32_t freed = 0;
     const uint32_t nv = held > 0 ? S.nv : 0u;
+#pragma unroll 1
     for (uint32_t j = 0; j < nv; ++j) {
       const uint4 mv = __ldcg(meta4 + j * 32 + lane_id());
       uint32_t nib = 0;
@@ -900,6 +942,7 @@ __device__ __noinline__ void op_touch(const Op op) {
     uint32_t* key = S.key;
     const uint4* meta4 = reinterpret_cast<const uint4*>(S.meta);
     const uint32_t nv = S.nv;
+#pragma unroll 1
     for (uint32_t j = 0; j < nv; ++j) {
       const uint4 mv = __ldcg(meta4 + j * 32 + lane_id());
       for (int e = 0; e < 4; ++e) {
@@ -948,7 +991,7 @@ __device__ __noinline__ void expiry() {
 // (P:1038-1041); materialized -> harmed when the predicate breaks without a
 // prior release (Table 4, G5)
 __device__ __noinline__ void post_op() {
-  need_tables(true, true);
+  need_both();
     const bool lc = lane_id() < S.C;
   const uint32_t w0 = S.cl[lane_id()][0];
   const uint32_t st = w0 & 0xFFu, mode = (w0 >> 8) & 0xFFu, o = (w0 >> 16) & 0xFFu;
@@ -1048,24 +1091,39 @@ __global__ void __launch_bounds__(256) rkc_light_kernel(const __grid_constant__ 
   if (blockIdx.x == 0 && threadIdx.x < 8) p.bcnt[((step + 1u) & 1u) * 8 + threadIdx.x] = 0;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t stride = gridDim.x * blockDim.x;
+  __shared__ uint32_t s_cnt[8], s_base[8];
+  if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
   for (uint32_t base = blockIdx.x * blockDim.x; base < p.num_traces; base += stride) {
     const uint32_t t = base + threadIdx.x;
     const bool valid = t < p.num_traces;
     bool heavy = false;
     uint32_t kind = 0;
     if (valid) {
+      // level 1: the op and the trace's hot header (independent of the op)
       const uint4 opw = __ldcs(args.ops + t);
+      const uint32_t* h = p.hdr + (size_t)t * H_NWORDS;
+      const uint4 hv0 = __ldcg(reinterpret_cast<const uint4*>(h));      // U, policy, accept, seq
+      const uint4 hv1 = __ldcg(reinterpret_cast<const uint4*>(h) + 1);  // free, alive, P, mask
+      const uint32_t nexp = __ldcg(h + H_NEXT_EXPIRY);
       kind = opw.x & 0xFFu;
       const uint32_t a = (opw.x >> 8) & 0xFFu;
-      const uint32_t* h = p.hdr + (size_t)t * H_NWORDS;
       heavy = true;
       if (kind == OP_NOP) {
-        heavy = step >= __ldcg(h + H_NEXT_EXPIRY);
+        heavy = step >= nexp;
       } else if (kind == OP_ADVANCE && a < p.Q) {
+        // level 2: the request record and (speculatively) the free bitmap
         uint32_t* rq = p.req + ((size_t)t * p.Q + a) * 8;
         const uint4 r0 = __ldcg(reinterpret_cast<const uint4*>(rq));
         const uint2 r1 = __ldcg(reinterpret_cast<const uint2*>(rq + 4));
-        const uint32_t nexp = __ldcg(h + H_NEXT_EXPIRY);
+        uint32_t* fbm = p.fbm + (size_t)t * (p.NS / 32);
+        const uint32_t nw4 = p.NS <= 1024 ? p.NS / 128 : 0u;
+        uint4 fw[8];
+#ifdef RKC_LIGHT_SPEC_FBM
+#pragma unroll
+        for (uint32_t q = 0; q < 8; ++q)
+          if (q < nw4) fw[q] = __ldcg(reinterpret_cast<const uint4*>(fbm) + q);
+#endif
         const uint32_t status = r0.x & 0xFFu, prompt = r0.y, chunk = r0.z, decode = r0.w;
         const uint32_t done = r1.x, live = r1.y;
         if (step < nexp && status == R_RUNNING && (uint64_t)done < (uint64_t)prompt + decode) {
@@ -1075,22 +1133,19 @@ __global__ void __launch_bounds__(256) rkc_light_kernel(const __grid_constant__ 
             rq[RQ_DONE] = done + n;
             atomicAdd(p.ctr + (size_t)t * K_NCTR + K_OPS, 1u);
             heavy = false;
-          } else if (p.NS <= 1024) {
+          } else if (nw4 > 0) {
             // a feasible allocation served entirely from free blocks: the
             // `need` lowest-id free blocks get positions live.. (G24); no
             // victim, no event, no claim or object change
             const uint32_t need = (uint32_t)(need_total - live);
-            const uint4 hv0 = __ldcg(reinterpret_cast<const uint4*>(h));      // U, policy, accept, seq
-            const uint4 hv1 = __ldcg(reinterpret_cast<const uint4*>(h) + 1);  // free, alive, P, mask
             if ((uint64_t)hv1.z + hv1.y + need <= hv0.x && need <= hv1.x) {
-              uint32_t* fbm = p.fbm + (size_t)t * (p.NS / 32);
               uint32_t* key = p.key + (size_t)t * p.NS;
               uint32_t* meta = p.meta + (size_t)t * p.NS;
-              const uint32_t nw4 = p.NS / 128;
-              uint4 fw[8];
+#ifndef RKC_LIGHT_SPEC_FBM
 #pragma unroll
               for (uint32_t q = 0; q < 8; ++q)
                 if (q < nw4) fw[q] = __ldcg(reinterpret_cast<const uint4*>(fbm) + q);
+#endif
               uint32_t taken = 0;
 #pragma unroll
               for (uint32_t q = 0; q < 8; ++q) {
@@ -1127,9 +1182,6 @@ __global__ void __launch_bounds__(256) rkc_light_kernel(const __grid_constant__ 
                  opw.y >= 1 && opw.z >= 1 && opw.y <= kMaxTokens && opw.w <= kMaxTokens) {
         uint32_t* rq = p.req + ((size_t)t * p.Q + a) * 8;
         const uint32_t status = __ldcg(rq) & 0xFFu;
-        const uint4 hv0 = __ldcg(reinterpret_cast<const uint4*>(h));       // U, policy, accept, seq
-        const uint4 hv1 = __ldcg(reinterpret_cast<const uint4*>(h) + 1);   // free, alive, P, mask
-        const uint32_t nexp = __ldcg(h + H_NEXT_EXPIRY);
         if (step < nexp && status != R_RUNNING && status != R_DEFERRED) {
           const uint64_t peak = ((uint64_t)opw.y + opw.w + kBlockTokens - 1) / kBlockTokens;
           const bool peak_check = ((hv0.y >> 8) & 0xFFu) == ADMIT_PEAK;
@@ -1146,26 +1198,34 @@ __global__ void __launch_bounds__(256) rkc_light_kernel(const __grid_constant__ 
         }
       }
     }
+    // bucket ranks: warp match -> CTA shared counts -> one global atomic per bucket per CTA
     const uint32_t bk = heavy ? bucket_of(kind) : 8u;
     const uint32_t grp = __match_any_sync(kFull, bk);
     const uint32_t leader = __ffs(grp) - 1;
     uint32_t off = 0;
-    if (lane == leader && heavy) off = atomicAdd(cnt + bk, __popc(grp));
+    if (lane == leader && heavy) off = atomicAdd(&s_cnt[bk], __popc(grp));
     off = __shfl_sync(kFull, off, leader);
-    if (heavy) p.perm[(size_t)bk * p.num_traces + off + __popc(grp & lanemask_lt())] = t;
+    __syncthreads();
+    if (threadIdx.x < 8) {
+      const uint32_t c = s_cnt[threadIdx.x];
+      s_base[threadIdx.x] = c ? atomicAdd(cnt + threadIdx.x, c) : 0u;
+      s_cnt[threadIdx.x] = 0;
+    }
+    __syncthreads();
+    if (heavy) p.perm[(size_t)bk * p.num_traces + s_base[bk] + off + __popc(grp & lanemask_lt())] = t;
   }
 }
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 32)
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 32 / kWarpsPerCta)
 rkc_step_kernel(const __grid_constant__ StepArgs args) {
   const uint32_t lane = threadIdx.x & 31u;
-  // CTA i -> the i-th trace of the op-kind bucketed order of this step
+  // warp w of CTA b -> the (b * kWarpsPerCta + w)-th trace of the op-kind bucketed order
   uint32_t t;
   {
     const uint4* cnt4 = reinterpret_cast<const uint4*>(args.p.bcnt + (args.step & 1u) * 8);
     const uint4 ca = __ldcg(cnt4), cb = __ldcg(cnt4 + 1);
     const uint32_t cnt[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
-    const uint32_t i = blockIdx.x;
+    const uint32_t i = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
     uint32_t acc = 0, bk = 8, off = 0;
 #pragma unroll
     for (uint32_t q = 0; q < 8; ++q) {
@@ -1258,17 +1318,15 @@ rkc_step_kernel(const __grid_constant__ StepArgs args) {
   finish();
 }
 
-extern std::atomic<unsigned long long> g_launches;
 
 // host launcher: one launch = one lockstep step over all traces
 cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, cudaStream_t st) {
-  g_launches += 1;
-  g_launches += 1;
   StepArgs args{p, reinterpret_cast<const uint4*>(ops_step), step};
   const uint32_t cgrid = (p.num_traces + 255) / 256 < 148 * 8 ? (p.num_traces + 255) / 256 : 148 * 8;
   rkc_light_kernel<<<cgrid, 256, 0, st>>>(args);
-  rkc_step_kernel<<<p.num_traces, kWarpsPerCta * 32, 0, st>>>(args);
+  rkc_step_kernel<<<(p.num_traces + kWarpsPerCta - 1) / kWarpsPerCta, kWarpsPerCta * 32, 0, st>>>(args);
   return cudaGetLastError();
 }
 
+}  // namespace RKC_STEP_NS
 }  // namespace rkc

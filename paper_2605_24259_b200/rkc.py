@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librkc.so")
+# RKC_LIB selects an alternative in-tree build of the same library (kernel A/B experiments)
+LIB_PATH = os.environ.get("RKC_LIB") or os.path.join(_HERE, "librkc.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

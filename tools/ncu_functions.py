@@ -13,7 +13,7 @@ import tempfile
 def func_ranges(lib):
     d = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=d, capture_output=True)
-    cub = [f for f in glob.glob(os.path.join(d, "*.cubin")) if os.path.basename(f).startswith("rkc_step.")][0]
+    cub = [f for f in glob.glob(os.path.join(d, "*.cubin")) if os.path.basename(f).startswith(os.environ.get("RKC_STEP_TU", "rkc_step_o64."))][0]
     out = subprocess.check_output(["readelf", "-sW", cub], text=True, stderr=subprocess.DEVNULL)
     rng = []
     sect = None
@@ -33,24 +33,27 @@ def func_ranges(lib):
 
 
 def main(rep, lib, dump=None):
-    out = subprocess.check_output(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                                  text=True)
+    out = subprocess.check_output(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
+                                   "-k", "regex:rkc_step_kernel", "-c", "1"], text=True)
     rows = list(csv.reader(out.splitlines()))
     hdr = rows[1]
     ai, ii, wi = hdr.index("Address"), hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
+    reasons = ["stall_long_sb", "stall_no_inst", "stall_wait", "stall_short_sb", "stall_branch_resolving"]
+    ri = [hdr.index(r) for r in reasons]
     data = []
     src = {}
     si = hdr.index("Source")
     for r in rows[2:]:
         try:
-            data.append((int(r[ai], 16), int(r[ii]), int(r[wi])))
+            data.append((int(r[ai], 16), int(r[ii]), int(r[wi]), [int(float(r[j] or 0)) for j in ri]))
             src[int(r[ai], 16)] = r[si].strip()
         except (ValueError, IndexError):
             break  # second kernel block starts
     base = data[0][0]
     rng = func_ranges(lib)
     inst, samp = collections.Counter(), collections.Counter()
-    for a, i, w in data:
+    rs = collections.defaultdict(lambda: [0] * len(reasons))
+    for a, i, w, st in data:
         off = a - base
         name = "kernel"
         for lo, hi, n in rng:
@@ -58,12 +61,13 @@ def main(rep, lib, dump=None):
                 name = n
         inst[name] += i
         samp[name] += w
+        rs[name] = [x + y for x, y in zip(rs[name], st)]
         if dump and name == dump:
-            print(f"{off:6x} {i:10d} {w:6d} {src[(a)]}")
+            print(f"{off:6x} {i:10d} {w:6d} {' '.join(f'{x:4d}' for x in st)} {src[(a)]}")
     ti, ts = sum(inst.values()), sum(samp.values())
-    print(f"{'function':24s} {'inst':>12s} {'inst%':>6s} {'samples%':>8s}")
+    print(f"{'function':24s} {'inst':>12s} {'inst%':>6s} {'samples%':>8s}  " + " ".join(r[6:14] for r in reasons))
     for n, s in samp.most_common():
-        print(f"{n:24s} {inst[n]:12d} {inst[n]/ti:6.3f} {s/ts:8.3f}")
+        print(f"{n:24s} {inst[n]:12d} {inst[n]/ti:6.3f} {s/ts:8.3f}  " + " ".join(f"{x/ts:8.3f}" for x in rs[n]))
 
 
 if __name__ == "__main__":

@@ -6,7 +6,7 @@ import subprocess
 import sys
 
 
-def main(rep, top=40, fname="rkc_step.cu"):
+def main(rep, top=40, fname="rkc_step_impl.cuh"):
     out = subprocess.check_output(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
                                    "cuda,sass"], text=True)
     inst, samp, text = collections.Counter(), collections.Counter(), {}
