@@ -1084,6 +1084,7 @@ __device__ __forceinline__ uint32_t bucket_of(uint32_t kind) {
 // with the exact effects the warp path would have (no events, no block, claim,
 // object or header change).  Every other trace is bucketed by op kind for the
 // warp-per-trace step kernel, heavy block-scanning kinds first.
+
 __global__ void __launch_bounds__(256) rkc_light_kernel(const __grid_constant__ StepArgs args) {
   const PoolDev& p = args.p;
   const uint32_t step = args.step;
@@ -1223,7 +1224,9 @@ rkc_step_kernel(const __grid_constant__ StepArgs args) {
   uint32_t t;
   {
     const uint4* cnt4 = reinterpret_cast<const uint4*>(args.p.bcnt + (args.step & 1u) * 8);
-    const uint4 ca = __ldcg(cnt4), cb = __ldcg(cnt4 + 1);
+    // read-only in this kernel and written by the previous one: the L1 path
+    // serves every CTA of an SM after the first (an L2 round trip each before)
+    const uint4 ca = __ldg(cnt4), cb = __ldg(cnt4 + 1);
     const uint32_t cnt[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
     const uint32_t i = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
     uint32_t acc = 0, bk = 8, off = 0;
@@ -1234,7 +1237,7 @@ rkc_step_kernel(const __grid_constant__ StepArgs args) {
       acc += c;
     }
     if (bk == 8) return;
-    t = __ldcg(args.p.perm + (size_t)bk * args.p.num_traces + off);
+    t = __ldg(args.p.perm + (size_t)bk * args.p.num_traces + off);
   }
   const PoolDev& p = args.p;
   const uint4 opw = __ldcs(args.ops + t);
