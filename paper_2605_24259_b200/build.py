@@ -8,8 +8,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = [os.path.join(CSRC, f) for f in ("rkc_step_o64.cu", "rkc_step_o128.cu", "rkc_abi.cu",
-                                           "rkc_conformance.cu")]
+SOURCES = [os.path.join(CSRC, f) for f in ("rkc_step_small_o64.cu", "rkc_step_small_o128.cu",
+                                           "rkc_step_big_o64.cu", "rkc_step_big_o128.cu",
+                                           "rkc_abi.cu", "rkc_conformance.cu")]
 HEADERS = [os.path.join(CSRC, f) for f in ("rkc_internal.cuh", "rkc_step_impl.cuh")] + \
     [os.path.join(ROOT, "include", "rkc.h")]
 LIB = os.path.join(HERE, "librkc.so")

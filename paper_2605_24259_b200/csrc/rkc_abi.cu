@@ -13,18 +13,23 @@
 #include "rkc_internal.cuh"
 
 namespace rkc {
-namespace o64 {
-cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, cudaStream_t st);
-}
-namespace o128 {
-cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, cudaStream_t st);
-}
+#define RKC_DECLARE_STEP(ns) \
+  namespace ns { cudaError_t launch_step(const PoolDev&, const void*, uint32_t, cudaStream_t); }
+RKC_DECLARE_STEP(small_o64)
+RKC_DECLARE_STEP(small_o128)
+RKC_DECLARE_STEP(big_o64)
+RKC_DECLARE_STEP(big_o128)
+#undef RKC_DECLARE_STEP
 std::atomic<unsigned long long> g_launches{0};  // kernels this library launched
 
-// one lockstep step = light pass + step kernel, from the build sized for the pool's object table
+// one lockstep step = light pass + step kernel, from the build of the pool's
+// size class: <= 1024 blocks (keys staged in shared memory) or more, and
+// <= 64 object slots (32 resident CTAs per SM) or up to 128
 static cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, cudaStream_t st) {
   g_launches += 2;
-  return p.O <= 64 ? o64::launch_step(p, ops_step, step, st) : o128::launch_step(p, ops_step, step, st);
+  if (p.NS <= 1024)
+    return p.O <= 64 ? small_o64::launch_step(p, ops_step, step, st) : small_o128::launch_step(p, ops_step, step, st);
+  return p.O <= 64 ? big_o64::launch_step(p, ops_step, step, st) : big_o128::launch_step(p, ops_step, step, st);
 }
 cudaError_t launch_conformance_array(const void* events, const uint32_t* offsets, uint32_t T,
                                      const uint8_t* final_states, uint32_t C, const uint8_t* lowering,

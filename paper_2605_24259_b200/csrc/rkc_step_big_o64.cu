@@ -1,0 +1,6 @@
+// rkc_step_big_o64.cu -- the step kernels (rkc_step_impl.cuh) for pools of more than 1024 blocks (block words streamed)
+// with at most 64 object slots.
+#define RKC_OMAX 64
+#define RKC_BIG 1
+#define RKC_STEP_NS big_o64
+#include "rkc_step_impl.cuh"

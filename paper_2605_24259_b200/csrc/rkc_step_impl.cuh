@@ -34,6 +34,14 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 // several warps holds its slot until its slowest trace is done)
 constexpr int kWarpsPerCta = RKC_WARPS_PER_CTA;
 constexpr uint32_t kStageMax = 1024;  // pools up to this size stage keys in smem
+// Pool-size class of this build (see rkc_step_*.cu): small pools (NS <=
+// kStageMax) stage their keys in shared memory and keep the block-scan loops
+// rolled (instruction cache); big pools stream their block words with
+// unrolled loops (loads in flight).
+#ifndef RKC_BIG
+#error "compile through rkc_step_{small,big}_o{64,128}.cu"
+#endif
+constexpr bool kBig = RKC_BIG;
 // Object slots held in shared memory.  This file is compiled twice
 // (rkc_step_o64.cu / rkc_step_o128.cu): pools with O <= 64 run the 64-slot
 // build, whose 6 KB warp state fits 32 resident CTAs per SM instead of 30.
@@ -270,6 +278,11 @@ __device__ __forceinline__ void add_protected(uint32_t o, uint32_t added) {
 }
 
 // ------------------------------ block passes -------------------------------
+template <int U, class F>
+__device__ __forceinline__ void for_vec(uint32_t nv, F&& f) {
+#pragma unroll U
+  for (uint32_t j = 0; j < nv; ++j) f(j);
+}
 __device__ __forceinline__ uint32_t block_of(uint32_t j, int e) {
   return (j * 32 + lane_id()) * 4 + e;
 }
@@ -282,6 +295,7 @@ __device__ __forceinline__ void fbm_set(uint32_t j, uint32_t nib) {
 
 // reclass pass: rewrite the class bits of every cached block whose owner is
 // marked, from the owner's bound claim; recount the protected blocks.
+template <bool big>
 __device__ __noinline__ void flush_reclass_pass() {
     prefetch_blocks(S.meta);
   need_both();
@@ -303,8 +317,10 @@ __device__ __noinline__ void flush_reclass_pass() {
   const uint4* meta4 = reinterpret_cast<const uint4*>(S.meta);
   const uint4* key4 = reinterpret_cast<const uint4*>(key);
   const uint32_t nv = S.nv;
-#pragma unroll 1
-  for (uint32_t j = 0; j < nv; ++j) {
+  // one vector of block words per lane-step: rolled for staged-size pools
+  // (instruction cache), unrolled for big ones (loads in flight); each
+  // variant is its own function so the small-pool path stays compact
+  auto vec_pass = [&](uint32_t j) {
     const uint4 mv = __ldcg(meta4 + j * 32 + lane_id());
     bool any = false;
 #pragma unroll
@@ -312,7 +328,7 @@ __device__ __noinline__ void flush_reclass_pass() {
       const uint32_t m = el(mv, e);
       any |= meta_res(m) == kResCached && in_reclass(meta_owner(m));
     }
-    if (!any) continue;
+    if (!any) return;
     const uint4 kv = __ldcg(key4 + j * 32 + lane_id());
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -327,7 +343,8 @@ __device__ __noinline__ void flush_reclass_pass() {
       if (k1 != k0) key[block_of(j, e)] = k1;
       if (cls == 3) atomicAdd(&S.cnt3[o], 1u);
     }
-  }
+  };
+  for_vec<big ? 4 : 1>(nv, vec_pass);
   __syncwarp();
   bool ch = false;
   if (lane_id() < S.C) {
@@ -344,19 +361,24 @@ __device__ __noinline__ void flush_reclass_pass() {
   refresh_protected();
 }
 __device__ __forceinline__ void flush_reclass() {
-  if (S.rc[0] | S.rc[1] | S.rc[2] | S.rc[3]) flush_reclass_pass();
+  if (S.rc[0] | S.rc[1] | S.rc[2] | S.rc[3]) {
+    flush_reclass_pass<kBig>();
+  }
 }
 
 // release request r's active blocks to FREE (deferral / refusal / no-admit)
-__device__ __noinline__ void release_blocks(uint32_t r) {
+template <bool big>
+__device__ __noinline__ void release_blocks_t(uint32_t r) {
   prefetch_blocks(S.meta);
   uint32_t* key = S.key;
   uint32_t* meta = S.meta;
   const uint4* meta4 = reinterpret_cast<const uint4*>(meta);
   uint32_t freed = 0;
   const uint32_t nv = S.nv;
-#pragma unroll 1
-  for (uint32_t j = 0; j < nv; ++j) {
+  // one vector of block words per lane-step: rolled for staged-size pools
+  // (instruction cache), unrolled for big ones (loads in flight); each
+  // variant is its own function so the small-pool path stays compact
+  auto vec_pass = [&](uint32_t j) {
     const uint4 mv = __ldcg(meta4 + j * 32 + lane_id());
     uint32_t nib = 0;
 #pragma unroll
@@ -375,9 +397,14 @@ __device__ __noinline__ void release_blocks(uint32_t r) {
       fbm_set(j, nib);
       freed += __popc(nib);
     }
-  }
+  };
+  for_vec<big ? 4 : 1>(nv, vec_pass);
   freed = __reduce_add_sync(kFull, freed);
   hset(H_FREE, S.h[H_FREE] + freed);
+}
+
+__device__ __forceinline__ void release_blocks(uint32_t r) {
+  release_blocks_t<kBig>(r);
 }
 
 // ------------------------------ arbiter ------------------------------------
@@ -459,7 +486,7 @@ template <bool staged>
 __device__ __noinline__ uint32_t count_le(uint32_t T) {
   uint32_t c = 0;
   const uint32_t nv = S.nv;
-#pragma unroll 1
+#pragma unroll(staged ? 1 : 4)
   for (uint32_t j = 0; j < nv; ++j) {
     const uint4 v = key_vec(j, staged);
     c += (v.x <= T) + (v.y <= T) + (v.z <= T) + (v.w <= T);
@@ -474,7 +501,7 @@ __device__ __noinline__ uint32_t min_class2() {
   constexpr uint32_t kC2 = 2u << kClassShift;
   uint32_t m2 = kFull;
   const uint32_t nv = S.nv;
-#pragma unroll 1
+#pragma unroll(staged ? 1 : 4)
   for (uint32_t j = 0; j < nv; ++j) {
     const uint4 v = key_vec(j, staged);
     m2 = min(min(m2, v.x - kC2), min(v.y - kC2, min(v.z - kC2, v.w - kC2)));
@@ -656,7 +683,7 @@ __device__ __noinline__ void alloc_evict(uint32_t k, uint32_t owner, bool insert
     __syncwarp();
     done_pos += n;
   };
-#pragma unroll 1
+#pragma unroll(staged ? 1 : 4)
   for (uint32_t j = 0; j < nv && done_pos + listed < k; ++j) {
     const uint4 v = key_vec(j, staged);
     const uint32_t tb = (v.x <= T ? 1u : 0u) | (v.y <= T ? 2u : 0u) | (v.z <= T ? 4u : 0u) |
@@ -702,8 +729,7 @@ __device__ __noinline__ void alloc(uint32_t k, uint32_t owner, bool insert,
   flush_reclass();
   if (insert) need_both();
   if (k <= S.h[H_FREE]) alloc_free(k, owner, insert, base);
-  else if (S.NS <= kStageMax) alloc_evict<true>(k, owner, insert, base);
-  else alloc_evict<false>(k, owner, insert, base);
+  else alloc_evict<!kBig>(k, owner, insert, base);
 }
 
 // ------------------------------ request io ---------------------------------
@@ -815,6 +841,7 @@ __device__ __noinline__ void op_advance(const Op op) {
 
 // COMPLETE: future reusable admission is separate from active allocation
 // (Table 7); only full blocks become reusable (G16).
+template <bool big>
 __device__ __noinline__ void op_complete(const Op op) {
     if (op.a >= S.Q) return op_error(op, ERR_INVALID_ARG);
   load_request(op.a);
@@ -845,8 +872,9 @@ __device__ __noinline__ void op_complete(const Op op) {
     const uint4* meta4 = reinterpret_cast<const uint4*>(meta);
     uint32_t freed = 0;
     const uint32_t nv = held > 0 ? S.nv : 0u;
-#pragma unroll 1
-    for (uint32_t j = 0; j < nv; ++j) {
+    // one vector of block words per lane-step: rolled for staged-size pools
+    // (instruction cache), unrolled for big ones (loads in flight)
+    auto vec_pass = [&](uint32_t j) {
       const uint4 mv = __ldcg(meta4 + j * 32 + lane_id());
       uint32_t nib = 0;
       for (int e = 0; e < 4; ++e) {
@@ -866,7 +894,8 @@ __device__ __noinline__ void op_complete(const Op op) {
       }
       fbm_set(j, nib);
       freed += __popc(nib);
-    }
+    };
+    for_vec<big ? 4 : 1>(nv, vec_pass);
     freed = __reduce_add_sync(kFull, freed);
     hset(H_FREE, S.h[H_FREE] + freed);
     hset(H_SEQ, seq_base + full);
@@ -931,6 +960,7 @@ __device__ __noinline__ void op_demote(const Op op) {
 
 // TOUCH: reuse probe of the materialization surface;
 // restamps the leading prefix tail-first (G23).
+template <bool big>
 __device__ __noinline__ void op_touch(const Op op) {
     if (op.a >= S.O) return op_error(op, ERR_INVALID_ARG);
   need_objs();
@@ -942,8 +972,9 @@ __device__ __noinline__ void op_touch(const Op op) {
     uint32_t* key = S.key;
     const uint4* meta4 = reinterpret_cast<const uint4*>(S.meta);
     const uint32_t nv = S.nv;
-#pragma unroll 1
-    for (uint32_t j = 0; j < nv; ++j) {
+    // one vector of block words per lane-step: rolled for staged-size pools
+    // (instruction cache), unrolled for big ones (loads in flight)
+    auto vec_pass = [&](uint32_t j) {
       const uint4 mv = __ldcg(meta4 + j * 32 + lane_id());
       for (int e = 0; e < 4; ++e) {
         const uint32_t m = el(mv, e);
@@ -952,7 +983,8 @@ __device__ __noinline__ void op_touch(const Op op) {
           key[bb] = (__ldcg(key + bb) & ~kSeqMask) | (seq_base + (L - 1 - meta_pos(m)));
         }
       }
-    }
+    };
+    for_vec<big ? 4 : 1>(nv, vec_pass);
     hset(H_SEQ, seq_base + L);
   }
   const uint32_t cc = obj_claim(ow);
@@ -1098,8 +1130,8 @@ __global__ void __launch_bounds__(256) rkc_light_kernel(const __grid_constant__ 
   for (uint32_t base = blockIdx.x * blockDim.x; base < p.num_traces; base += stride) {
     const uint32_t t = base + threadIdx.x;
     const bool valid = t < p.num_traces;
-    bool heavy = false;
-    uint32_t kind = 0;
+    bool heavy = false, fa = false;
+    uint32_t kind = 0, fa_need = 0, fa_live = 0, fa_owner = 0;
     if (valid) {
       // level 1: the op and the trace's hot header (independent of the op)
       const uint4 opw = __ldcs(args.ops + t);
@@ -1117,14 +1149,7 @@ __global__ void __launch_bounds__(256) rkc_light_kernel(const __grid_constant__ 
         uint32_t* rq = p.req + ((size_t)t * p.Q + a) * 8;
         const uint4 r0 = __ldcg(reinterpret_cast<const uint4*>(rq));
         const uint2 r1 = __ldcg(reinterpret_cast<const uint2*>(rq + 4));
-        uint32_t* fbm = p.fbm + (size_t)t * (p.NS / 32);
-        const uint32_t nw4 = p.NS <= 1024 ? p.NS / 128 : 0u;
-        uint4 fw[8];
-#ifdef RKC_LIGHT_SPEC_FBM
-#pragma unroll
-        for (uint32_t q = 0; q < 8; ++q)
-          if (q < nw4) fw[q] = __ldcg(reinterpret_cast<const uint4*>(fbm) + q);
-#endif
+        const bool small = p.NS <= 1024;  // one bitmap word per lane
         const uint32_t status = r0.x & 0xFFu, prompt = r0.y, chunk = r0.z, decode = r0.w;
         const uint32_t done = r1.x, live = r1.y;
         if (step < nexp && status == R_RUNNING && (uint64_t)done < (uint64_t)prompt + decode) {
@@ -1134,40 +1159,16 @@ __global__ void __launch_bounds__(256) rkc_light_kernel(const __grid_constant__ 
             rq[RQ_DONE] = done + n;
             atomicAdd(p.ctr + (size_t)t * K_NCTR + K_OPS, 1u);
             heavy = false;
-          } else if (nw4 > 0) {
+          } else if (small) {
             // a feasible allocation served entirely from free blocks: the
             // `need` lowest-id free blocks get positions live.. (G24); no
             // victim, no event, no claim or object change
             const uint32_t need = (uint32_t)(need_total - live);
             if ((uint64_t)hv1.z + hv1.y + need <= hv0.x && need <= hv1.x) {
-              uint32_t* key = p.key + (size_t)t * p.NS;
-              uint32_t* meta = p.meta + (size_t)t * p.NS;
-#ifndef RKC_LIGHT_SPEC_FBM
-#pragma unroll
-              for (uint32_t q = 0; q < 8; ++q)
-                if (q < nw4) fw[q] = __ldcg(reinterpret_cast<const uint4*>(fbm) + q);
-#endif
-              uint32_t taken = 0;
-#pragma unroll
-              for (uint32_t q = 0; q < 8; ++q) {
-                if (q >= nw4 || taken >= need) break;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  uint32_t word = el(fw[q], e);
-                  if (taken >= need || word == 0) continue;
-                  uint32_t tw = 0;
-                  while (word && taken < need) {
-                    const uint32_t bit = __ffs(word) - 1;
-                    word &= word - 1;
-                    tw |= 1u << bit;
-                    const uint32_t b = (q * 4 + e) * 32 + bit;
-                    meta[b] = meta_make(kResActive, a, live + taken);
-                    key[b] = kKeyActive;
-                    ++taken;
-                  }
-                  fbm[q * 4 + e] = el(fw[q], e) & ~tw;
-                }
-              }
+              fa = true;  // the blocks are taken warp-cooperatively below
+              fa_need = need;
+              fa_live = live;
+              fa_owner = a;
               uint32_t* hw = const_cast<uint32_t*>(h);
               hw[H_FREE] = hv1.x - need;
               hw[H_ALIVE] = hv1.y + need;
@@ -1196,6 +1197,30 @@ __global__ void __launch_bounds__(256) rkc_light_kernel(const __grid_constant__ 
             atomicAdd(p.ctr + (size_t)t * K_NCTR + K_ADMITTED, 1u);
             heavy = false;
           }
+        }
+      }
+    }
+    // free-only allocations, one trace at a time across the warp (lane = free
+    // bitmap word): the `need` lowest-id free blocks, positions live.. in
+    // block-id order (G24)
+    for (uint32_t fm = __ballot_sync(kFull, fa); fm; fm &= fm - 1) {
+      const uint32_t src = __ffs(fm) - 1;
+      const uint32_t tt = __shfl_sync(kFull, t, src), need = __shfl_sync(kFull, fa_need, src);
+      const uint32_t live = __shfl_sync(kFull, fa_live, src), owner = __shfl_sync(kFull, fa_owner, src);
+      uint32_t* fbm = p.fbm + (size_t)tt * (p.NS / 32);
+      const uint32_t word = lane < p.NS / 32 ? __ldcg(fbm + lane) : 0u;
+      const uint32_t c = __popc(word);
+      const uint32_t before = warp_incl_scan(c, lane) - c;
+      const uint32_t take = before >= need ? 0u : min(c, need - before);
+      if (take > 0) {
+        uint32_t tw = take == c ? word : word & ((1u << nth_set_bit(word, take + 1)) - 1u);
+        fbm[lane] = word & ~tw;
+        uint32_t* key = p.key + (size_t)tt * p.NS;
+        uint32_t* meta = p.meta + (size_t)tt * p.NS;
+        for (uint32_t r = live + before; tw; tw &= tw - 1, ++r) {
+          const uint32_t b = lane * 32 + __ffs(tw) - 1;
+          meta[b] = meta_make(kResActive, owner, r);
+          key[b] = kKeyActive;
         }
       }
     }
@@ -1311,10 +1336,10 @@ rkc_step_kernel(const __grid_constant__ StepArgs args) {
     case OP_SUBMIT: op_submit(op); break;
     case OP_ADMIT: op_admit(op); break;
     case OP_ADVANCE: op_advance(op); break;
-    case OP_COMPLETE: op_complete(op); break;
+    case OP_COMPLETE: op_complete<kBig>(op); break;
     case OP_INSERT: op_insert(op); break;
     case OP_DEMOTE: op_demote(op); break;
-    case OP_TOUCH: op_touch(op); break;
+    case OP_TOUCH: op_touch<kBig>(op); break;
     default: op_error(op, ERR_UNKNOWN_OP); break;
   }
   __syncwarp();

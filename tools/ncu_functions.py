@@ -13,13 +13,13 @@ import tempfile
 def func_ranges(lib):
     d = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=d, capture_output=True)
-    cub = [f for f in glob.glob(os.path.join(d, "*.cubin")) if os.path.basename(f).startswith(os.environ.get("RKC_STEP_TU", "rkc_step_o64."))][0]
+    cub = [f for f in glob.glob(os.path.join(d, "*.cubin")) if os.path.basename(f).startswith(os.environ.get("RKC_STEP_TU", "rkc_step_small_o64."))][0]
     out = subprocess.check_output(["readelf", "-sW", cub], text=True, stderr=subprocess.DEVNULL)
     rng = []
     sect = None
     for line in out.splitlines():
         f = line.split()
-        if len(f) >= 8 and f[3] == "FUNC" and f[-1].endswith("rkc_step_kernelENS_8StepArgsE"):
+        if len(f) >= 8 and f[3] == "FUNC" and "rkc_step_kernel" in f[-1] and "$" not in f[-1]:
             sect = f[-2]
     for line in out.splitlines():
         f = line.split()
@@ -27,7 +27,7 @@ def func_ranges(lib):
             off = int(f[1], 16)
             size = int(f[2], 16) if f[2].startswith("0x") else int(f[2])
             name = f[-1].split("$")[-1]
-            m = re.search(r"_ZN3rkc\d+(\w+?)E", name)
+            m = re.search(r"_ZN3rkc(?:3o\d+)?\d+(\w+?)E", name)
             rng.append((off, off + size, m.group(1) if m else name))
     return sorted(rng)
 
