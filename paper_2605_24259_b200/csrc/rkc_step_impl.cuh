@@ -42,6 +42,17 @@ constexpr uint32_t kStageMax = 1024;  // pools up to this size stage keys in sme
 #error "compile through rkc_step_{small,big}_o{64,128}.cu"
 #endif
 constexpr bool kBig = RKC_BIG;
+// Big pools run one CTA of kCrew warps per trace: warp 0 (the leader) runs the
+// op path exactly as in the small build; its block passes are split into
+// contiguous vector slices, one per warp of the crew (section "crew" below).
+#ifndef RKC_CREW
+#define RKC_CREW 8
+#endif
+constexpr uint32_t kCrew = kBig ? RKC_CREW : 1;
+#ifndef RKC_CREW_UNROLL
+#define RKC_CREW_UNROLL 2
+#endif
+constexpr int kCrewUnroll = RKC_CREW_UNROLL;  // block vectors in flight per lane in a crew pass
 // Object slots held in shared memory.  This file is compiled twice
 // (rkc_step_o64.cu / rkc_step_o128.cu): pools with O <= 64 run the 64-slot
 // build, whose 6 KB warp state fits 32 resident CTAs per SM instead of 30.
@@ -73,6 +84,10 @@ struct alignas(16) Warp {      // the warp's shared memory (one warp per CTA)
   alignas(16) uint32_t cl[32][8];  // claim records (lane c owns claim c)
   uint32_t obj0[kObjMax];      // object word 0
   uint32_t lead[kObjMax];      // leading prefix per object
+#if RKC_BIG
+  uint32_t job[8];             // crew job: kind, arguments
+  uint32_t red[kCrew][4];      // crew partial results, one row per warp
+#endif
   union alignas(16) {
     struct { uint32_t lim3[128], lim2[128], cnt3[128]; };  // reclass scratch
     uint32_t keys[kStageMax];  // staged selection keys (alloc only)
@@ -293,11 +308,309 @@ __device__ __forceinline__ void fbm_set(uint32_t j, uint32_t nib) {
   }
 }
 
+// ------------------------------ crew (big pools) ----------------------------
+// Warp w of the CTA owns block vectors [nv*w/kCrew, nv*(w+1)/kCrew) (block-id
+// order is preserved across warps).  The leader posts a job in S.job and all
+// warps run their slice between two named barriers; per-warp results land in
+// S.red[w].  Helpers (warps 1..) loop on jobs until JOB_EXIT.
+#if RKC_BIG
+enum : uint32_t { JOB_EXIT = 0, JOB_STATS, JOB_COUNT, JOB_MIN2, JOB_APPLY, JOB_RELEASE,
+                  JOB_COMPLETE, JOB_TOUCH, JOB_RECLASS, JOB_FREE_COUNT, JOB_FREE_TAKE };
+
+__device__ __forceinline__ void crew_bar() {
+  asm volatile("bar.sync 1, %0;" ::"r"(kCrew * 32) : "memory");
+}
+__device__ __forceinline__ uint32_t crew_j0(uint32_t w) { return S.nv * w / kCrew; }
+
+// one job's slice for warp w (lane = lane_id()); arguments in S.job[1..7]
+__device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
+  const uint32_t lane = lane_id();
+  const uint32_t j0 = crew_j0(w), j1 = crew_j0(w + 1);
+  uint32_t* key = S.key;
+  uint32_t* meta = S.meta;
+  const uint4* key4 = reinterpret_cast<const uint4*>(key);
+  const uint4* meta4 = reinterpret_cast<const uint4*>(meta);
+  constexpr uint32_t kC1 = 1u << kClassShift;
+  uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+  switch (kind) {
+    case JOB_STATS: {  // class-1 count, smallest non-free key - 2^30 (see alloc_evict)
+      uint32_t md = kFull;
+#pragma unroll(kCrewUnroll)
+      for (uint32_t j = j0; j < j1; ++j) {
+        const uint4 v = __ldcg(key4 + j * 32 + lane);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t d = el(v, e) - kC1;
+          r0 += d < kC1 ? 1u : 0u;
+          md = min(md, d);
+        }
+      }
+      r0 = __reduce_add_sync(kFull, r0);
+      r1 = __reduce_min_sync(kFull, md);
+      break;
+    }
+    case JOB_COUNT: {  // #{key <= T}
+      const uint32_t T = S.job[1];
+#pragma unroll(kCrewUnroll)
+      for (uint32_t j = j0; j < j1; ++j) {
+        const uint4 v = __ldcg(key4 + j * 32 + lane);
+        r0 += (v.x <= T) + (v.y <= T) + (v.z <= T) + (v.w <= T);
+      }
+      r0 = __reduce_add_sync(kFull, r0);
+      break;
+    }
+    case JOB_MIN2: {  // smallest class-2 key - 2^31
+      constexpr uint32_t kC2 = 2u << kClassShift;
+      uint32_t m2 = kFull;
+#pragma unroll(kCrewUnroll)
+      for (uint32_t j = j0; j < j1; ++j) {
+        const uint4 v = __ldcg(key4 + j * 32 + lane);
+        m2 = min(min(m2, v.x - kC2), min(v.y - kC2, min(v.z - kC2, v.w - kC2)));
+      }
+      r0 = __reduce_min_sync(kFull, m2);
+      break;
+    }
+    case JOB_APPLY: {  // take {key <= T}: ranks continue from the warps before (counts at T in red[.][0])
+      const uint32_t T = S.job[1], base = S.job[2], owner = S.job[3] & 0x7FFFFFFFu;
+      const bool insert = S.job[3] >> 31;
+      const uint32_t k = S.job[4], l3 = S.job[5], l2 = S.job[6], seq_base = S.job[7];
+      uint32_t rank = 0;
+      for (uint32_t v = 0; v < w; ++v) rank += S.red[v][0];
+      const uint32_t end = rank + S.red[w][0];
+      for (uint32_t j = j0; j < j1 && rank < end; ++j) {
+        const uint4 v = __ldcg(key4 + j * 32 + lane);
+        const uint32_t tb = (v.x <= T ? 1u : 0u) | (v.y <= T ? 2u : 0u) | (v.z <= T ? 4u : 0u) |
+                            (v.w <= T ? 8u : 0u);
+        if (!__any_sync(kFull, tb != 0)) continue;
+        const uint32_t cnt = __popc(tb);
+        const uint32_t Sc = warp_incl_scan(cnt, lane);
+        uint32_t r = rank + Sc - cnt;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (!((tb >> e) & 1u)) continue;
+          const uint32_t bb = block_of(j, e);
+          const uint32_t pos = base + r++;
+          if (el(v, e) >= kC1) {  // a victim: attributed by its object's claim now (Table 4)
+            const uint32_t m = __ldcg(meta + bb);
+            const uint32_t o = meta_owner(m);
+            const uint32_t cc = obj_claim(S.obj0[o]);
+            const uint32_t st = cc < 32 ? cl_state(cc) : C_EMPTY;
+            if (st == C_DEMOTED || st == C_EXPIRED) ++r2;
+            else if (st == C_ACCEPTED || st == C_MATERIALIZED) ++r3;
+            else ++r1;
+            atomicMin(&S.lead[o], meta_pos(m));
+            atomicOr(&S.objdirty[o >> 5], 1u << (o & 31u));
+          }
+          if (insert) {
+            const uint32_t cls = pos < l3 ? 3u : (pos < l2 ? 2u : 1u);
+            key[bb] = (cls << kClassShift) | (seq_base + (k - 1 - pos));
+            meta[bb] = meta_make(kResCached, owner, pos);
+          } else {
+            key[bb] = kKeyActive;
+            meta[bb] = meta_make(kResActive, owner, pos);
+          }
+        }
+        rank += __shfl_sync(kFull, Sc, 31);
+      }
+      for (uint32_t wi = j0 * 4 + lane; wi < j1 * 4; wi += 32) S.fbm[wi] = 0;  // every free block was taken
+      r1 = __reduce_add_sync(kFull, r1);
+      r2 = __reduce_add_sync(kFull, r2);
+      r3 = __reduce_add_sync(kFull, r3);
+      break;
+    }
+    case JOB_RELEASE: {  // request S.job[1]'s active blocks -> FREE
+      const uint32_t rq = S.job[1];
+#pragma unroll(kCrewUnroll)
+      for (uint32_t j = j0; j < j1; ++j) {
+        const uint4 mv = __ldcg(meta4 + j * 32 + lane);
+        uint32_t nib = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t m = el(mv, e);
+          if (meta_res(m) == kResActive && meta_owner(m) == rq) nib |= 1u << e;
+        }
+        if (nib) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (!((nib >> e) & 1u)) continue;
+            const uint32_t bb = block_of(j, e);
+            meta[bb] = meta_make(kResFree, 0, 0);
+            key[bb] = bb;
+          }
+          fbm_set(j, nib);
+          r0 += __popc(nib);
+        }
+      }
+      r0 = __reduce_add_sync(kFull, r0);
+      break;
+    }
+    case JOB_COMPLETE: {  // request a's blocks: full ones -> CACHED(o) tail-first stamps, rest -> FREE
+      const uint32_t a = S.job[1], full = S.job[2], o = S.job[3], lim3 = S.job[4], lim2 = S.job[5];
+      const uint32_t seq_base = S.job[6];
+#pragma unroll(kCrewUnroll)
+      for (uint32_t j = j0; j < j1; ++j) {
+        const uint4 mv = __ldcg(meta4 + j * 32 + lane);
+        uint32_t nib = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t m = el(mv, e);
+          if (meta_res(m) != kResActive || meta_owner(m) != a) continue;
+          const uint32_t bb = block_of(j, e);
+          const uint32_t pos = meta_pos(m);
+          if (pos < full) {
+            const uint32_t cls = pos < lim3 ? 3u : (pos < lim2 ? 2u : 1u);
+            key[bb] = (cls << kClassShift) | (seq_base + (full - 1 - pos));
+            meta[bb] = meta_make(kResCached, o, pos);
+          } else {
+            key[bb] = bb;
+            meta[bb] = meta_make(kResFree, 0, 0);
+            nib |= 1u << e;
+          }
+        }
+        fbm_set(j, nib);
+        r0 += __popc(nib);
+      }
+      r0 = __reduce_add_sync(kFull, r0);
+      break;
+    }
+    case JOB_TOUCH: {  // restamp object S.job[1]'s leading prefix [0, L) tail-first
+      const uint32_t ob = S.job[1], L = S.job[2], seq_base = S.job[3];
+#pragma unroll(kCrewUnroll)
+      for (uint32_t j = j0; j < j1; ++j) {
+        const uint4 mv = __ldcg(meta4 + j * 32 + lane);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t m = el(mv, e);
+          if (meta_res(m) == kResCached && meta_owner(m) == ob && meta_pos(m) < L) {
+            const uint32_t bb = block_of(j, e);
+            key[bb] = (__ldcg(key + bb) & ~kSeqMask) | (seq_base + (L - 1 - meta_pos(m)));
+          }
+        }
+      }
+      break;
+    }
+    case JOB_RECLASS: {  // class bits of the marked objects' cached blocks (S.lim3 / S.lim2 / S.cnt3)
+#pragma unroll(kCrewUnroll)
+      for (uint32_t j = j0; j < j1; ++j) {
+        const uint4 mv = __ldcg(meta4 + j * 32 + lane);
+        bool any = false;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t m = el(mv, e);
+          any |= meta_res(m) == kResCached && in_reclass(meta_owner(m));
+        }
+        if (!any) continue;
+        const uint4 kv = __ldcg(key4 + j * 32 + lane);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t m = el(mv, e);
+          if (meta_res(m) != kResCached) continue;
+          const uint32_t o = meta_owner(m);
+          if (!in_reclass(o)) continue;
+          const uint32_t pos = meta_pos(m);
+          const uint32_t cls = pos < S.lim3[o] ? 3u : (pos < S.lim2[o] ? 2u : 1u);
+          const uint32_t k0 = el(kv, e);
+          const uint32_t k1 = (cls << kClassShift) | (k0 & kSeqMask);
+          if (k1 != k0) key[block_of(j, e)] = k1;
+          if (cls == 3) atomicAdd(&S.cnt3[o], 1u);
+        }
+      }
+      break;
+    }
+    case JOB_FREE_COUNT: {  // free blocks in the slice's bitmap words
+      for (uint32_t wi = j0 * 4 + lane; wi < j1 * 4; wi += 32) r0 += __popc(__ldcg(S.fbm + wi));
+      r0 = __reduce_add_sync(kFull, r0);
+      break;
+    }
+    case JOB_FREE_TAKE: {  // the k lowest-id free blocks: ranks continue from the warps before
+      const uint32_t k = S.job[1], owner = S.job[2] & 0x7FFFFFFFu, base = S.job[3];
+      const bool insert = S.job[2] >> 31;
+      const uint32_t l3 = S.job[4], l2 = S.job[5], seq_base = S.job[6];
+      uint32_t acc = 0;
+      for (uint32_t v = 0; v < w; ++v) acc += S.red[v][0];
+      for (uint32_t w0 = j0 * 4; w0 < j1 * 4 && acc < k; w0 += 32) {
+        const uint32_t wi = w0 + lane;
+        const uint32_t word = wi < j1 * 4 ? __ldcg(S.fbm + wi) : 0u;
+        const uint32_t c = __popc(word);
+        const uint32_t Sc = warp_incl_scan(c, lane);
+        const uint32_t before = acc + Sc - c;
+        const uint32_t take = before >= k ? 0u : min(c, k - before);
+        if (take > 0) {
+          uint32_t tw = take == c ? word : word & ((1u << nth_set_bit(word, take + 1)) - 1u);
+          S.fbm[wi] = word & ~tw;
+          for (uint32_t r = before; tw; tw &= tw - 1, ++r) {
+            const uint32_t bb = wi * 32 + __ffs(tw) - 1;
+            const uint32_t pos = base + r;
+            if (insert) {
+              const uint32_t cls = pos < l3 ? 3u : (pos < l2 ? 2u : 1u);
+              key[bb] = (cls << kClassShift) | (seq_base + (k - 1 - pos));
+              meta[bb] = meta_make(kResCached, owner, pos);
+            } else {
+              key[bb] = kKeyActive;
+              meta[bb] = meta_make(kResActive, owner, pos);
+            }
+          }
+        }
+        acc += __shfl_sync(kFull, Sc, 31);
+      }
+      break;
+    }
+    default:
+      break;
+  }
+  if (lane == 0) { S.red[w][0] = (kind == JOB_APPLY || kind == JOB_FREE_TAKE) ? S.red[w][0] : r0; S.red[w][1] = r1; S.red[w][2] = r2; S.red[w][3] = r3; }
+}
+
+// leader: run a job (arguments already in S.job[1..]) across the crew
+__device__ __noinline__ void crew_run(uint32_t kind) {
+  __syncwarp();
+  if (lane_id() == 0) S.job[0] = kind;
+  crew_bar();  // start: the helpers read the job
+  crew_work(kind, 0);
+  crew_bar();  // end: every partial result is in S.red
+}
+__device__ __forceinline__ uint32_t crew_sum(uint32_t c) {
+  uint32_t s = 0;
+#pragma unroll
+  for (uint32_t w = 0; w < kCrew; ++w) s += S.red[w][c];
+  return s;
+}
+__device__ __forceinline__ uint32_t crew_min(uint32_t c) {
+  uint32_t s = kFull;
+#pragma unroll
+  for (uint32_t w = 0; w < kCrew; ++w) s = min(s, S.red[w][c]);
+  return s;
+}
+__device__ __forceinline__ void job_args(uint32_t a1, uint32_t a2 = 0, uint32_t a3 = 0, uint32_t a4 = 0,
+                                         uint32_t a5 = 0, uint32_t a6 = 0, uint32_t a7 = 0) {
+  if (lane_id() == 0) {
+    S.job[1] = a1; S.job[2] = a2; S.job[3] = a3; S.job[4] = a4; S.job[5] = a5; S.job[6] = a6; S.job[7] = a7;
+  }
+}
+__device__ __noinline__ void crew_helper() {
+  const uint32_t w = threadIdx.x >> 5;
+  for (;;) {
+    crew_bar();
+    const uint32_t kind = S.job[0];
+    if (kind == JOB_EXIT) return;
+    crew_work(kind, w);
+    crew_bar();
+  }
+}
+__device__ __forceinline__ void crew_exit() {
+  __syncwarp();
+  if (lane_id() == 0) S.job[0] = JOB_EXIT;
+  crew_bar();
+}
+#else
+__device__ __forceinline__ void crew_exit() {}
+#endif
+
 // reclass pass: rewrite the class bits of every cached block whose owner is
 // marked, from the owner's bound claim; recount the protected blocks.
 template <bool big>
 __device__ __noinline__ void flush_reclass_pass() {
-    prefetch_blocks(S.meta);
+  if (!big) prefetch_blocks(S.meta);
   need_both();
   const uint32_t low = lowering();
   for (uint32_t o = lane_id(); o < S.O; o += 32) {
@@ -344,7 +657,11 @@ __device__ __noinline__ void flush_reclass_pass() {
       if (cls == 3) atomicAdd(&S.cnt3[o], 1u);
     }
   };
-  for_vec<big ? 4 : 1>(nv, vec_pass);
+#if RKC_BIG
+  if constexpr (big) crew_run(JOB_RECLASS);
+  else
+#endif
+    for_vec<big ? 4 : 1>(nv, vec_pass);
   __syncwarp();
   bool ch = false;
   if (lane_id() < S.C) {
@@ -369,6 +686,14 @@ __device__ __forceinline__ void flush_reclass() {
 // release request r's active blocks to FREE (deferral / refusal / no-admit)
 template <bool big>
 __device__ __noinline__ void release_blocks_t(uint32_t r) {
+#if RKC_BIG
+  if constexpr (big) {
+    job_args(r);
+    crew_run(JOB_RELEASE);
+    hset(H_FREE, S.h[H_FREE] + crew_sum(0));
+    return;
+  }
+#endif
   prefetch_blocks(S.meta);
   uint32_t* key = S.key;
   uint32_t* meta = S.meta;
@@ -484,6 +809,13 @@ __device__ __forceinline__ uint4 key_vec(uint32_t j, bool staged) {
 }
 template <bool staged>
 __device__ __noinline__ uint32_t count_le(uint32_t T) {
+#if RKC_BIG
+  if constexpr (!staged) {
+    job_args(T);
+    crew_run(JOB_COUNT);
+    return crew_sum(0);
+  }
+#endif
   uint32_t c = 0;
   const uint32_t nv = S.nv;
 #pragma unroll(staged ? 1 : 4)
@@ -499,6 +831,12 @@ __device__ __noinline__ uint32_t count_le(uint32_t T) {
 template <bool staged>
 __device__ __noinline__ uint32_t min_class2() {
   constexpr uint32_t kC2 = 2u << kClassShift;
+#if RKC_BIG
+  if constexpr (!staged) {
+    crew_run(JOB_MIN2);
+    return crew_min(0) + kC2;
+  }
+#endif
   uint32_t m2 = kFull;
   const uint32_t nv = S.nv;
 #pragma unroll(staged ? 1 : 4)
@@ -527,6 +865,14 @@ __device__ __noinline__ void alloc_free(uint32_t k, uint32_t owner, bool insert,
       if (cls == 2) l2 = S.cl[cc][CF_F];
     }
   }
+#if RKC_BIG
+  crew_run(JOB_FREE_COUNT);
+  job_args(k, owner | (insert ? 0x80000000u : 0u), base, l3, l2, seq_base);
+  crew_run(JOB_FREE_TAKE);
+  hset(H_FREE, S.h[H_FREE] - k);
+  ctr_add(K_BLOCKS_ALLOCATED, k);
+  return;
+#endif
   uint32_t acc = 0;
   for (uint32_t w0 = 0; w0 < nw && acc < k; w0 += 32) {
     const uint32_t wi = w0 + lane_id();
@@ -603,7 +949,13 @@ __device__ __noinline__ void alloc_evict(uint32_t k, uint32_t owner, bool insert
     __syncwarp();
   } else {
     need_both();
+#if RKC_BIG
+    crew_run(JOB_STATS);
+    c1 = lane_id() == 0 ? crew_sum(0) : 0u;  // summed over the warp below
+    md = crew_min(1);
+#else
     for (uint32_t j = 0; j < nv; ++j) stat(__ldcg(key4 + j * 32 + lane));
+#endif
   }
   c1 = __reduce_add_sync(kFull, c1);
   uint32_t lo, clo, top;
@@ -652,60 +1004,69 @@ __device__ __noinline__ void alloc_evict(uint32_t k, uint32_t owner, bool insert
     }
   }
   uint32_t ord = 0, rel = 0, clm = 0;
-  uint32_t listed = 0, done_pos = 0;
-  auto drain = [&](uint32_t n) {
-#pragma unroll 1
-    for (uint32_t i = lane_id(); i < n; i += 32) {
-      const uint32_t e = list[i];
-      const uint32_t bb = e & 0x7FFFFFFFu;
-      const uint32_t rank = done_pos + i;
-      const uint32_t pos = base + rank;
-      if (e >> 31) {
-        const uint32_t m = __ldcg(meta + bb);
-        const uint32_t o = meta_owner(m);
-        const uint32_t cc = obj_claim(S.obj0[o]);
-        const uint32_t st = cc < 32 ? cl_state(cc) : C_EMPTY;
-        if (st == C_DEMOTED || st == C_EXPIRED) ++rel;
-        else if (st == C_ACCEPTED || st == C_MATERIALIZED) ++clm;
-        else ++ord;
-        atomicMin(&S.lead[o], meta_pos(m));
-        atomicOr(&S.objdirty[o >> 5], 1u << (o & 31u));
-      }
-      if (insert) {
-        const uint32_t cls = pos < l3 ? 3u : (pos < l2 ? 2u : 1u);
-        key[bb] = (cls << kClassShift) | (seq_base + (k - 1 - pos));
-        meta[bb] = meta_make(kResCached, owner, pos);
-      } else {
-        key[bb] = kKeyActive;
-        meta[bb] = meta_make(kResActive, owner, pos);
-      }
-    }
-    __syncwarp();
-    done_pos += n;
-  };
-#pragma unroll(staged ? 1 : 4)
-  for (uint32_t j = 0; j < nv && done_pos + listed < k; ++j) {
-    const uint4 v = key_vec(j, staged);
-    const uint32_t tb = (v.x <= T ? 1u : 0u) | (v.y <= T ? 2u : 0u) | (v.z <= T ? 4u : 0u) |
-                        (v.w <= T ? 8u : 0u);
-    if (!__any_sync(kFull, tb != 0)) continue;
-    const uint32_t cnt = __popc(tb);
-    const uint32_t Sc = warp_incl_scan(cnt, lane_id());
-    const uint32_t tot = __shfl_sync(kFull, Sc, 31);
-    if (!staged && listed + tot > kStageMax) { drain(listed); listed = 0; }
-    uint32_t r = listed + Sc - cnt;
-    if (tb & 1u) list[r++] = block_of(j, 0) | (v.x >= (1u << kClassShift) ? 0x80000000u : 0u);
-    if (tb & 2u) list[r++] = block_of(j, 1) | (v.y >= (1u << kClassShift) ? 0x80000000u : 0u);
-    if (tb & 4u) list[r++] = block_of(j, 2) | (v.z >= (1u << kClassShift) ? 0x80000000u : 0u);
-    if (tb & 8u) list[r++] = block_of(j, 3) | (v.w >= (1u << kClassShift) ? 0x80000000u : 0u);
-    listed += tot;
-    __syncwarp();
-  }
-  drain(listed);
-  // every free block was taken
+#if RKC_BIG
+  if constexpr (!staged) {  // each crew warp takes its slice's keys <= T (ranks from the last count)
+    job_args(T, base, owner | (insert ? 0x80000000u : 0u), k, l3, l2, seq_base);
+    crew_run(JOB_APPLY);
+    if (lane_id() == 0) { ord = crew_sum(1); rel = crew_sum(2); clm = crew_sum(3); }
+  } else
+#endif
   {
-    uint32_t* fb = S.fbm;
-    for (uint32_t wi = lane_id(); wi < nv * 4; wi += 32) fb[wi] = 0;
+    uint32_t listed = 0, done_pos = 0;
+    auto drain = [&](uint32_t n) {
+#pragma unroll 1
+      for (uint32_t i = lane_id(); i < n; i += 32) {
+        const uint32_t e = list[i];
+        const uint32_t bb = e & 0x7FFFFFFFu;
+        const uint32_t rank = done_pos + i;
+        const uint32_t pos = base + rank;
+        if (e >> 31) {
+          const uint32_t m = __ldcg(meta + bb);
+          const uint32_t o = meta_owner(m);
+          const uint32_t cc = obj_claim(S.obj0[o]);
+          const uint32_t st = cc < 32 ? cl_state(cc) : C_EMPTY;
+          if (st == C_DEMOTED || st == C_EXPIRED) ++rel;
+          else if (st == C_ACCEPTED || st == C_MATERIALIZED) ++clm;
+          else ++ord;
+          atomicMin(&S.lead[o], meta_pos(m));
+          atomicOr(&S.objdirty[o >> 5], 1u << (o & 31u));
+        }
+        if (insert) {
+          const uint32_t cls = pos < l3 ? 3u : (pos < l2 ? 2u : 1u);
+          key[bb] = (cls << kClassShift) | (seq_base + (k - 1 - pos));
+          meta[bb] = meta_make(kResCached, owner, pos);
+        } else {
+          key[bb] = kKeyActive;
+          meta[bb] = meta_make(kResActive, owner, pos);
+        }
+      }
+      __syncwarp();
+      done_pos += n;
+    };
+#pragma unroll(staged ? 1 : 4)
+    for (uint32_t j = 0; j < nv && done_pos + listed < k; ++j) {
+      const uint4 v = key_vec(j, staged);
+      const uint32_t tb = (v.x <= T ? 1u : 0u) | (v.y <= T ? 2u : 0u) | (v.z <= T ? 4u : 0u) |
+                          (v.w <= T ? 8u : 0u);
+      if (!__any_sync(kFull, tb != 0)) continue;
+      const uint32_t cnt = __popc(tb);
+      const uint32_t Sc = warp_incl_scan(cnt, lane_id());
+      const uint32_t tot = __shfl_sync(kFull, Sc, 31);
+      if (!staged && listed + tot > kStageMax) { drain(listed); listed = 0; }
+      uint32_t r = listed + Sc - cnt;
+      if (tb & 1u) list[r++] = block_of(j, 0) | (v.x >= (1u << kClassShift) ? 0x80000000u : 0u);
+      if (tb & 2u) list[r++] = block_of(j, 1) | (v.y >= (1u << kClassShift) ? 0x80000000u : 0u);
+      if (tb & 4u) list[r++] = block_of(j, 2) | (v.z >= (1u << kClassShift) ? 0x80000000u : 0u);
+      if (tb & 8u) list[r++] = block_of(j, 3) | (v.w >= (1u << kClassShift) ? 0x80000000u : 0u);
+      listed += tot;
+      __syncwarp();
+    }
+    drain(listed);
+    // every free block was taken
+    {
+      uint32_t* fb = S.fbm;
+      for (uint32_t wi = lane_id(); wi < nv * 4; wi += 32) fb[wi] = 0;
+    }
   }
   ord = __reduce_add_sync(kFull, ord);
   rel = __reduce_add_sync(kFull, rel);
@@ -895,7 +1256,16 @@ __device__ __noinline__ void op_complete(const Op op) {
       fbm_set(j, nib);
       freed += __popc(nib);
     };
-    for_vec<big ? 4 : 1>(nv, vec_pass);
+#if RKC_BIG
+    if constexpr (big) {
+      if (nv) {
+        job_args(op.a, full, o, cls_lim3, cls_lim2, seq_base);
+        crew_run(JOB_COMPLETE);
+        freed = lane_id() == 0 ? crew_sum(0) : 0u;
+      }
+    } else
+#endif
+      for_vec<big ? 4 : 1>(nv, vec_pass);
     freed = __reduce_add_sync(kFull, freed);
     hset(H_FREE, S.h[H_FREE] + freed);
     hset(H_SEQ, seq_base + full);
@@ -984,7 +1354,13 @@ __device__ __noinline__ void op_touch(const Op op) {
         }
       }
     };
-    for_vec<big ? 4 : 1>(nv, vec_pass);
+#if RKC_BIG
+    if constexpr (big) {
+      job_args(op.a, L, seq_base);
+      crew_run(JOB_TOUCH);
+    } else
+#endif
+      for_vec<big ? 4 : 1>(nv, vec_pass);
     hset(H_SEQ, seq_base + L);
   }
   const uint32_t cc = obj_claim(ow);
@@ -1242,7 +1618,7 @@ __global__ void __launch_bounds__(256) rkc_light_kernel(const __grid_constant__ 
   }
 }
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 32 / kWarpsPerCta)
+__global__ void __launch_bounds__(kWarpsPerCta * kCrew * 32, 32 / (kWarpsPerCta * kCrew))
 rkc_step_kernel(const __grid_constant__ StepArgs args) {
   const uint32_t lane = threadIdx.x & 31u;
   // warp w of CTA b -> the (b * kWarpsPerCta + w)-th trace of the op-kind bucketed order
@@ -1253,7 +1629,7 @@ rkc_step_kernel(const __grid_constant__ StepArgs args) {
     // serves every CTA of an SM after the first (an L2 round trip each before)
     const uint4 ca = __ldg(cnt4), cb = __ldg(cnt4 + 1);
     const uint32_t cnt[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
-    const uint32_t i = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+    const uint32_t i = blockIdx.x * kWarpsPerCta + (kWarpsPerCta == 1 ? 0u : (threadIdx.x >> 5));
     uint32_t acc = 0, bk = 8, off = 0;
 #pragma unroll
     for (uint32_t q = 0; q < 8; ++q) {
@@ -1264,6 +1640,12 @@ rkc_step_kernel(const __grid_constant__ StepArgs args) {
     if (bk == 8) return;
     t = __ldg(args.p.perm + (size_t)bk * args.p.num_traces + off);
   }
+#if RKC_BIG
+  if (threadIdx.x >= 32) {  // crew helpers: block-pass slices until the leader is done
+    crew_helper();
+    return;
+  }
+#endif
   const PoolDev& p = args.p;
   const uint4 opw = __ldcs(args.ops + t);
   const uint32_t kind = opw.x & 0xFFu, a = (opw.x >> 8) & 0xFFu;
@@ -1289,7 +1671,9 @@ rkc_step_kernel(const __grid_constant__ StepArgs args) {
     for (int i = 0; i < 4; ++i)
       if (lane + 32 * i < p.O) ov[i] = __ldcg(obase + lane + 32 * i);
   }
-  if (kind == OP_COMPLETE || kind == OP_TOUCH) {  // these ops scan the block words
+  if (kBig) {
+    // big pools: the crew streams the block words itself
+  } else if (kind == OP_COMPLETE || kind == OP_TOUCH) {  // these ops scan the block words
     const uint32_t* mb = p.meta + (size_t)t * p.NS;
     for (uint32_t l = lane; l < p.NS / 32; l += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(mb + l * 32));
   } else if (kind == OP_ADVANCE || kind == OP_INSERT) {  // heavy ones allocate: keys next
@@ -1298,7 +1682,10 @@ rkc_step_kernel(const __grid_constant__ StepArgs args) {
   }
   const uint32_t next_exp = __shfl_sync(kFull, hw, H_NEXT_EXPIRY);
   // a NOP with no expiry due changes nothing (fast path)
-  if (kind == OP_NOP && args.step < next_exp) return;
+  if (kind == OP_NOP && args.step < next_exp) {
+    crew_exit();
+    return;
+  }
   if (lane < H_NWORDS) S.h[lane] = hw;
   S.ctr[lane] = 0;
   if (lane < 4) { S.rc[lane] = 0; S.objdirty[lane] = 0; }
@@ -1344,6 +1731,7 @@ rkc_step_kernel(const __grid_constant__ StepArgs args) {
   }
   __syncwarp();
   finish();
+  crew_exit();
 }
 
 
@@ -1352,7 +1740,7 @@ cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, c
   StepArgs args{p, reinterpret_cast<const uint4*>(ops_step), step};
   const uint32_t cgrid = (p.num_traces + 255) / 256 < 148 * 8 ? (p.num_traces + 255) / 256 : 148 * 8;
   rkc_light_kernel<<<cgrid, 256, 0, st>>>(args);
-  rkc_step_kernel<<<(p.num_traces + kWarpsPerCta - 1) / kWarpsPerCta, kWarpsPerCta * 32, 0, st>>>(args);
+  rkc_step_kernel<<<(p.num_traces + kWarpsPerCta - 1) / kWarpsPerCta, kWarpsPerCta * kCrew * 32, 0, st>>>(args);
   return cudaGetLastError();
 }
 
