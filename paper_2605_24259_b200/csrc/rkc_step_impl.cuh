@@ -1618,28 +1618,28 @@ __global__ void __launch_bounds__(256) rkc_light_kernel(const __grid_constant__ 
   }
 }
 
-__global__ void __launch_bounds__(kWarpsPerCta * kCrew * 32, 32 / (kWarpsPerCta * kCrew))
-rkc_step_kernel(const __grid_constant__ StepArgs args) {
-  const uint32_t lane = threadIdx.x & 31u;
-  // warp w of CTA b -> the (b * kWarpsPerCta + w)-th trace of the op-kind bucketed order
-  uint32_t t;
-  {
-    const uint4* cnt4 = reinterpret_cast<const uint4*>(args.p.bcnt + (args.step & 1u) * 8);
-    // read-only in this kernel and written by the previous one: the L1 path
-    // serves every CTA of an SM after the first (an L2 round trip each before)
-    const uint4 ca = __ldg(cnt4), cb = __ldg(cnt4 + 1);
-    const uint32_t cnt[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
-    const uint32_t i = blockIdx.x * kWarpsPerCta + (kWarpsPerCta == 1 ? 0u : (threadIdx.x >> 5));
-    uint32_t acc = 0, bk = 8, off = 0;
+// bucketed item i of this step -> its trace (false past the heavy count)
+__device__ __forceinline__ bool item_trace(const StepArgs& args, uint32_t i, uint32_t& t) {
+  const uint4* cnt4 = reinterpret_cast<const uint4*>(args.p.bcnt + (args.step & 1u) * 8);
+  // read-only in this kernel and written by the previous one: the L1 path
+  // serves every CTA of an SM after the first (an L2 round trip each before)
+  const uint4 ca = __ldg(cnt4), cb = __ldg(cnt4 + 1);
+  const uint32_t cnt[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+  uint32_t acc = 0, bk = 8, off = 0;
 #pragma unroll
-    for (uint32_t q = 0; q < 8; ++q) {
-      const uint32_t c = cnt[q];
-      if (bk == 8 && i < acc + c) { bk = q; off = i - acc; }
-      acc += c;
-    }
-    if (bk == 8) return;
-    t = __ldg(args.p.perm + (size_t)bk * args.p.num_traces + off);
+  for (uint32_t q = 0; q < 8; ++q) {
+    const uint32_t c = cnt[q];
+    if (bk == 8 && i < acc + c) { bk = q; off = i - acc; }
+    acc += c;
   }
+  if (bk == 8) return false;
+  t = __ldg(args.p.perm + (size_t)bk * args.p.num_traces + off);
+  return true;
+}
+
+// one heavy trace-step of trace t: the warp's whole op path
+__device__ __forceinline__ void run_item(const StepArgs& args, uint32_t t) {
+  const uint32_t lane = threadIdx.x & 31u;
 #if RKC_BIG
   if (threadIdx.x >= 32) {  // crew helpers: block-pass slices until the leader is done
     crew_helper();
@@ -1734,13 +1734,51 @@ rkc_step_kernel(const __grid_constant__ StepArgs args) {
   crew_exit();
 }
 
+// K1: warp w of CTA b -> the (b * kWarpsPerCta + w)-th trace of the op-kind
+// bucketed order.  Small pools launch CTAs for the first kMainItems(T) items
+// only (the heavy share of a step is about half); the rest, if any, run on
+// the overflow kernel below.
+__global__ void __launch_bounds__(kWarpsPerCta * kCrew * 32, 32 / (kWarpsPerCta * kCrew))
+rkc_step_kernel(const __grid_constant__ StepArgs args) {
+  uint32_t t;
+  if (!item_trace(args, blockIdx.x * kWarpsPerCta + (kWarpsPerCta == 1 ? 0u : (threadIdx.x >> 5)), t)) return;
+  run_item(args, t);
+}
+
+#if !RKC_BIG
+#ifndef RKC_MAIN_SIXTEENTHS
+#define RKC_MAIN_SIXTEENTHS 10
+#endif
+__host__ __device__ constexpr uint32_t kMainItems(uint32_t T) {  // RKC_MAIN_SIXTEENTHS/16 of T
+  return (uint32_t)(((uint64_t)T * RKC_MAIN_SIXTEENTHS + 15) / 16);
+}
+// items [kMainItems(T), heavy count), if any: a grid of 1/16 of the remaining
+// slots (at least 592 CTAs) loops over them, at most 16 items per warp -- a
+// step with more heavy traces than the main grid slows down gradually
+__host__ __device__ constexpr uint32_t kOverflowCtas(uint32_t T) {
+  return (T - kMainItems(T)) / 16 > 592 ? (T - kMainItems(T)) / 16 : 592;
+}
+__global__ void __launch_bounds__(32) rkc_step_overflow_kernel(const __grid_constant__ StepArgs args) {
+  for (uint32_t i = kMainItems(args.p.num_traces) + blockIdx.x;; i += gridDim.x) {
+    uint32_t t;
+    if (!item_trace(args, i, t)) return;
+    run_item(args, t);
+    __syncwarp();
+  }
+}
+#endif
 
 // host launcher: one launch = one lockstep step over all traces
 cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, cudaStream_t st) {
   StepArgs args{p, reinterpret_cast<const uint4*>(ops_step), step};
   const uint32_t cgrid = (p.num_traces + 255) / 256 < 148 * 8 ? (p.num_traces + 255) / 256 : 148 * 8;
   rkc_light_kernel<<<cgrid, 256, 0, st>>>(args);
+#if RKC_BIG
   rkc_step_kernel<<<(p.num_traces + kWarpsPerCta - 1) / kWarpsPerCta, kWarpsPerCta * kCrew * 32, 0, st>>>(args);
+#else
+  rkc_step_kernel<<<(kMainItems(p.num_traces) + kWarpsPerCta - 1) / kWarpsPerCta, kWarpsPerCta * 32, 0, st>>>(args);
+  rkc_step_overflow_kernel<<<kOverflowCtas(p.num_traces), 32, 0, st>>>(args);
+#endif
   return cudaGetLastError();
 }
 
