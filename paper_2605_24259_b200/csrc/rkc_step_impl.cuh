@@ -101,6 +101,19 @@ __shared__ Warp S_[kWarpsPerCta];
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
+// Programmatic dependent launch: one step = light pass -> step kernel ->
+// overflow kernel -> next light pass, each launched with programmatic stream
+// serialisation, so a kernel is launched as its predecessor's last CTAs exit
+// instead of after the full kernel boundary; it waits for the predecessor's
+// completion and memory (griddepcontrol.wait) before touching trace state.
+// (An explicit early trigger at CTA start measured slower: the successor's
+// CTAs then sit in SM slots the predecessor's tail could use.)
+__device__ __forceinline__ void pdl_wait() {
+#ifndef RKC_NO_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 struct Op { uint32_t kind, a, b, c, x, y, z; };
 
 // ------------------------------ helpers ------------------------------------
@@ -1497,6 +1510,7 @@ __global__ void __launch_bounds__(256) rkc_light_kernel(const __grid_constant__ 
   const PoolDev& p = args.p;
   const uint32_t step = args.step;
   uint32_t* cnt = p.bcnt + (step & 1u) * 8;
+  pdl_wait();
   if (blockIdx.x == 0 && threadIdx.x < 8) p.bcnt[((step + 1u) & 1u) * 8 + threadIdx.x] = 0;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t stride = gridDim.x * blockDim.x;
@@ -1740,6 +1754,7 @@ __device__ __forceinline__ void run_item(const StepArgs& args, uint32_t t) {
 // the overflow kernel below.
 __global__ void __launch_bounds__(kWarpsPerCta * kCrew * 32, 32 / (kWarpsPerCta * kCrew))
 rkc_step_kernel(const __grid_constant__ StepArgs args) {
+  pdl_wait();
   uint32_t t;
   if (!item_trace(args, blockIdx.x * kWarpsPerCta + (kWarpsPerCta == 1 ? 0u : (threadIdx.x >> 5)), t)) return;
   run_item(args, t);
@@ -1759,6 +1774,7 @@ __host__ __device__ constexpr uint32_t kOverflowCtas(uint32_t T) {
   return (T - kMainItems(T)) / 16 > 592 ? (T - kMainItems(T)) / 16 : 592;
 }
 __global__ void __launch_bounds__(32) rkc_step_overflow_kernel(const __grid_constant__ StepArgs args) {
+  pdl_wait();
   for (uint32_t i = kMainItems(args.p.num_traces) + blockIdx.x;; i += gridDim.x) {
     uint32_t t;
     if (!item_trace(args, i, t)) return;
@@ -1768,18 +1784,36 @@ __global__ void __launch_bounds__(32) rkc_step_overflow_kernel(const __grid_cons
 }
 #endif
 
+template <class Kernel>
+static cudaError_t launch_pdl(Kernel kernel, uint32_t grid, uint32_t block, cudaStream_t st,
+                              const StepArgs& args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args);
+}
+
 // host launcher: one launch = one lockstep step over all traces
 cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, cudaStream_t st) {
   StepArgs args{p, reinterpret_cast<const uint4*>(ops_step), step};
   const uint32_t cgrid = (p.num_traces + 255) / 256 < 148 * 8 ? (p.num_traces + 255) / 256 : 148 * 8;
-  rkc_light_kernel<<<cgrid, 256, 0, st>>>(args);
+  cudaError_t e = launch_pdl(rkc_light_kernel, cgrid, 256, st, args);
 #if RKC_BIG
-  rkc_step_kernel<<<(p.num_traces + kWarpsPerCta - 1) / kWarpsPerCta, kWarpsPerCta * kCrew * 32, 0, st>>>(args);
+  if (e == cudaSuccess)
+    e = launch_pdl(rkc_step_kernel, (p.num_traces + kWarpsPerCta - 1) / kWarpsPerCta, kWarpsPerCta * kCrew * 32, st, args);
 #else
-  rkc_step_kernel<<<(kMainItems(p.num_traces) + kWarpsPerCta - 1) / kWarpsPerCta, kWarpsPerCta * 32, 0, st>>>(args);
-  rkc_step_overflow_kernel<<<kOverflowCtas(p.num_traces), 32, 0, st>>>(args);
+  if (e == cudaSuccess)
+    e = launch_pdl(rkc_step_kernel, (kMainItems(p.num_traces) + kWarpsPerCta - 1) / kWarpsPerCta, kWarpsPerCta * 32, st, args);
+  if (e == cudaSuccess) e = launch_pdl(rkc_step_overflow_kernel, kOverflowCtas(p.num_traces), 32, st, args);
 #endif
-  return cudaGetLastError();
+  return e;
 }
 
 }  // namespace RKC_STEP_NS
