@@ -162,8 +162,9 @@ def load_peak() -> tuple[float, str]:
 
 
 def load_traffic() -> float | None:
-    """dram bytes per step-kernel launch from the committed ncu --set full capture."""
-    p = os.path.join(ROOT, "profiles", "ncu_step_kernel.json")
+    """dram bytes per lockstep step from the committed ncu --set full capture of this workload."""
+    name = "ncu_step_kernel.json" if WL is WORKLOADS["c3"] else f"ncu_step_kernel_{WL['desc'][:2]}.json"
+    p = os.path.join(ROOT, "profiles", name)
     try:
         return float(json.load(open(p))["dram_bytes_per_launch"])
     except Exception:
@@ -374,7 +375,8 @@ def main():
         "events_per_step": total_events,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "rkc_step_kernel", "peak_source": peak_src,
+                     "kernel": "lockstep step: rkc_light_kernel + rkc_step_kernel + rkc_step_overflow_kernel",
+                     "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": ab["bytes"] / TSTEPS,
                      "avg_launch_us": per_launch_ms * 1e3,
                      "step_kernel_share": step_kernel_ms / ms},
