@@ -1506,7 +1506,11 @@ __device__ __forceinline__ uint32_t bucket_of(uint32_t kind) {
 // object or header change).  Every other trace is bucketed by op kind for the
 // warp-per-trace step kernel, heavy block-scanning kinds first.
 
-__global__ void __launch_bounds__(256) rkc_light_kernel(const __grid_constant__ StepArgs args) {
+#ifndef RKC_LIGHT_THREADS
+#define RKC_LIGHT_THREADS 128
+#endif
+constexpr uint32_t kLightThreads = RKC_LIGHT_THREADS;
+__global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_constant__ StepArgs args) {
   const PoolDev& p = args.p;
   const uint32_t step = args.step;
   uint32_t* cnt = p.bcnt + (step & 1u) * 8;
@@ -1593,12 +1597,28 @@ __global__ void __launch_bounds__(256) rkc_light_kernel(const __grid_constant__ 
     // free-only allocations, one trace at a time across the warp (lane = free
     // bitmap word): the `need` lowest-id free blocks, positions live.. in
     // block-id order (G24)
-    for (uint32_t fm = __ballot_sync(kFull, fa); fm; fm &= fm - 1) {
-      const uint32_t src = __ffs(fm) - 1;
+    // (the bitmap words of up to 8 traces are loaded before any is consumed)
+    for (uint32_t fm = __ballot_sync(kFull, fa); fm;) {
+      uint32_t words[8], srcs[8], nb = 0;
+#pragma unroll
+      for (uint32_t q = 0; q < 8; ++q) {
+        srcs[q] = fm ? __ffs(fm) - 1 : 0u;
+        words[q] = 0;
+        if (fm) {
+          const uint32_t tq = __shfl_sync(kFull, t, srcs[q]);
+          if (lane < p.NS / 32) words[q] = __ldcg(p.fbm + (size_t)tq * (p.NS / 32) + lane);
+          fm &= fm - 1;
+          nb = q + 1;
+        }
+      }
+#pragma unroll
+      for (uint32_t q = 0; q < 8; ++q) {
+      if (q >= nb) break;
+      const uint32_t src = srcs[q];
       const uint32_t tt = __shfl_sync(kFull, t, src), need = __shfl_sync(kFull, fa_need, src);
       const uint32_t live = __shfl_sync(kFull, fa_live, src), owner = __shfl_sync(kFull, fa_owner, src);
       uint32_t* fbm = p.fbm + (size_t)tt * (p.NS / 32);
-      const uint32_t word = lane < p.NS / 32 ? __ldcg(fbm + lane) : 0u;
+      const uint32_t word = words[q];
       const uint32_t c = __popc(word);
       const uint32_t before = warp_incl_scan(c, lane) - c;
       const uint32_t take = before >= need ? 0u : min(c, need - before);
@@ -1612,6 +1632,7 @@ __global__ void __launch_bounds__(256) rkc_light_kernel(const __grid_constant__ 
           meta[b] = meta_make(kResActive, owner, r);
           key[b] = kKeyActive;
         }
+      }
       }
     }
     // bucket ranks: warp match -> CTA shared counts -> one global atomic per bucket per CTA
@@ -1685,14 +1706,13 @@ __device__ __forceinline__ void run_item(const StepArgs& args, uint32_t t) {
     for (int i = 0; i < 4; ++i)
       if (lane + 32 * i < p.O) ov[i] = __ldcg(obase + lane + 32 * i);
   }
-  if (kBig) {
-    // big pools: the crew streams the block words itself
-  } else if (kind == OP_COMPLETE || kind == OP_TOUCH) {  // these ops scan the block words
-    const uint32_t* mb = p.meta + (size_t)t * p.NS;
-    for (uint32_t l = lane; l < p.NS / 32; l += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(mb + l * 32));
-  } else if (kind == OP_ADVANCE || kind == OP_INSERT) {  // heavy ones allocate: keys next
-    const uint32_t* kb = p.key + (size_t)t * p.NS;
-    for (uint32_t l = lane; l < p.NS / 32; l += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(kb + l * 32));
+  // small pools: one 128-B line of the block words per lane (NS <= 1024); big
+  // pools: the crew streams the block words itself
+  if (!kBig && lane < p.NS / 32) {
+    const bool scan = kind == OP_COMPLETE || kind == OP_TOUCH;  // these ops scan the block words
+    const bool sel = kind == OP_ADVANCE || kind == OP_INSERT;   // heavy ones allocate: keys next
+    if (scan) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.meta + (size_t)t * p.NS + lane * 32));
+    if (sel) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.key + (size_t)t * p.NS + lane * 32));
   }
   const uint32_t next_exp = __shfl_sync(kFull, hw, H_NEXT_EXPIRY);
   // a NOP with no expiry due changes nothing (fast path)
@@ -1803,8 +1823,9 @@ static cudaError_t launch_pdl(Kernel kernel, uint32_t grid, uint32_t block, cuda
 // host launcher: one launch = one lockstep step over all traces
 cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, cudaStream_t st) {
   StepArgs args{p, reinterpret_cast<const uint4*>(ops_step), step};
-  const uint32_t cgrid = (p.num_traces + 255) / 256 < 148 * 8 ? (p.num_traces + 255) / 256 : 148 * 8;
-  cudaError_t e = launch_pdl(rkc_light_kernel, cgrid, 256, st, args);
+  const uint32_t lct = (p.num_traces + kLightThreads - 1) / kLightThreads;
+  const uint32_t cgrid = lct < 148 * 2048 / kLightThreads ? lct : 148 * 2048 / kLightThreads;
+  cudaError_t e = launch_pdl(rkc_light_kernel, cgrid, kLightThreads, st, args);
 #if RKC_BIG
   if (e == cudaSuccess)
     e = launch_pdl(rkc_step_kernel, (p.num_traces + kWarpsPerCta - 1) / kWarpsPerCta, kWarpsPerCta * kCrew * 32, st, args);
