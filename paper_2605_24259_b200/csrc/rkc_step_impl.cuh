@@ -311,6 +311,22 @@ __device__ __forceinline__ void for_vec(uint32_t nv, F&& f) {
 #pragma unroll U
   for (uint32_t j = 0; j < nv; ++j) f(j);
 }
+// small pools: the block meta words, all loads in flight at once, into the
+// staging buffer (the scans then run rolled over shared memory)
+__device__ __forceinline__ const uint4* stage_meta() {
+  const uint4* meta4 = reinterpret_cast<const uint4*>(S.meta);
+  uint4* st = reinterpret_cast<uint4*>(S.keys);
+  const uint32_t nv = S.nv, lane = lane_id();
+  uint4 mv[kStageMax / 128];
+#pragma unroll
+  for (uint32_t j = 0; j < kStageMax / 128; ++j)
+    if (j < nv) mv[j] = __ldcg(meta4 + j * 32 + lane);
+#pragma unroll
+  for (uint32_t j = 0; j < kStageMax / 128; ++j)
+    if (j < nv) st[j * 32 + lane] = mv[j];
+  __syncwarp();
+  return st;
+}
 __device__ __forceinline__ uint32_t block_of(uint32_t j, int e) {
   return (j * 32 + lane_id()) * 4 + e;
 }
@@ -707,17 +723,16 @@ __device__ __noinline__ void release_blocks_t(uint32_t r) {
     return;
   }
 #endif
-  prefetch_blocks(S.meta);
   uint32_t* key = S.key;
   uint32_t* meta = S.meta;
-  const uint4* meta4 = reinterpret_cast<const uint4*>(meta);
+  const uint4* meta4 = stage_meta();
   uint32_t freed = 0;
   const uint32_t nv = S.nv;
   // one vector of block words per lane-step: rolled for staged-size pools
   // (instruction cache), unrolled for big ones (loads in flight); each
   // variant is its own function so the small-pool path stays compact
   auto vec_pass = [&](uint32_t j) {
-    const uint4 mv = __ldcg(meta4 + j * 32 + lane_id());
+    const uint4 mv = meta4[j * 32 + lane_id()];
     uint32_t nib = 0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -1243,13 +1258,13 @@ __device__ __noinline__ void op_complete(const Op op) {
     const uint32_t seq_base = S.h[H_SEQ];
     uint32_t* key = S.key;
     uint32_t* meta = S.meta;
-    const uint4* meta4 = reinterpret_cast<const uint4*>(meta);
     uint32_t freed = 0;
     const uint32_t nv = held > 0 ? S.nv : 0u;
-    // one vector of block words per lane-step: rolled for staged-size pools
-    // (instruction cache), unrolled for big ones (loads in flight)
+    const uint4* meta4 = (big || nv == 0) ? reinterpret_cast<const uint4*>(meta) : stage_meta();
+    // small pools: one staged vector of block words per lane-step, rolled
+    // (instruction cache); big pools run the crew job below
     auto vec_pass = [&](uint32_t j) {
-      const uint4 mv = __ldcg(meta4 + j * 32 + lane_id());
+      const uint4 mv = meta4[j * 32 + lane_id()];
       uint32_t nib = 0;
       for (int e = 0; e < 4; ++e) {
         const uint32_t m = el(mv, e);
@@ -1353,17 +1368,30 @@ __device__ __noinline__ void op_touch(const Op op) {
   const uint32_t seq_base = S.h[H_SEQ];
   if (L > 0) {
     uint32_t* key = S.key;
-    const uint4* meta4 = reinterpret_cast<const uint4*>(S.meta);
     const uint32_t nv = S.nv;
-    // one vector of block words per lane-step: rolled for staged-size pools
-    // (instruction cache), unrolled for big ones (loads in flight)
+    const uint4* meta4 = big ? reinterpret_cast<const uint4*>(S.meta) : stage_meta();
+    // the class bits of the restamped blocks follow from the object's bound
+    // claim (the invariant the reclass pass maintains; a pending reclass of
+    // this object rewrites them to the same value), so no key is read back
+    uint32_t l3 = 0, l2 = 0;
+    if (!big) {
+      const uint32_t cc = obj_claim(ow);
+      if (cc < 32) need_claims();
+      if (cc < 32 && live_state(cl_state(cc))) {
+        const uint32_t cls = claim_class(cl_mode(cc), lowering());
+        if (cls == 3) l3 = S.cl[cc][CF_F];
+        if (cls == 2) l2 = S.cl[cc][CF_F];
+      }
+    }
+    // small pools: one staged vector per lane-step, rolled; big: the crew job
     auto vec_pass = [&](uint32_t j) {
-      const uint4 mv = __ldcg(meta4 + j * 32 + lane_id());
+      const uint4 mv = meta4[j * 32 + lane_id()];
       for (int e = 0; e < 4; ++e) {
         const uint32_t m = el(mv, e);
         if (meta_res(m) == kResCached && meta_owner(m) == op.a && meta_pos(m) < L) {
-          const uint32_t bb = block_of(j, e);
-          key[bb] = (__ldcg(key + bb) & ~kSeqMask) | (seq_base + (L - 1 - meta_pos(m)));
+          const uint32_t pos = meta_pos(m);
+          const uint32_t cls = pos < l3 ? 3u : (pos < l2 ? 2u : 1u);
+          key[block_of(j, e)] = (cls << kClassShift) | (seq_base + (L - 1 - pos));
         }
       }
     };
