@@ -100,7 +100,7 @@ struct PoolDev {
   uint32_t* obj;    // [T][O][2]
   uint32_t* ctr;    // [T][32]
   uint4* ev;        // [T][EPT][2]
-  uint32_t* perm;   // [8][T] traces bucketed by op kind for the current step
+  uint32_t* perm;   // [8][T] 64-B tickets {op, hot header, trace}: heavy trace-steps by op kind
   uint32_t* bcnt;   // [2][8] bucket sizes (double-buffered by step parity)
 };
 

@@ -1554,13 +1554,15 @@ __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_c
     const bool valid = t < p.num_traces;
     bool heavy = false, fa = false;
     uint32_t kind = 0, fa_need = 0, fa_live = 0, fa_owner = 0;
+    uint4 opw = make_uint4(0, 0, 0, 0), hv0 = opw, hv1 = opw, hv2 = opw;
     if (valid) {
       // level 1: the op and the trace's hot header (independent of the op)
-      const uint4 opw = __ldcs(args.ops + t);
+      opw = __ldcs(args.ops + t);
       const uint32_t* h = p.hdr + (size_t)t * H_NWORDS;
-      const uint4 hv0 = __ldcg(reinterpret_cast<const uint4*>(h));      // U, policy, accept, seq
-      const uint4 hv1 = __ldcg(reinterpret_cast<const uint4*>(h) + 1);  // free, alive, P, mask
-      const uint32_t nexp = __ldcg(h + H_NEXT_EXPIRY);
+      hv0 = __ldcg(reinterpret_cast<const uint4*>(h));      // U, policy, accept, seq
+      hv1 = __ldcg(reinterpret_cast<const uint4*>(h) + 1);  // free, alive, P, mask
+      hv2 = __ldcg(reinterpret_cast<const uint4*>(h) + 2);  // next expiry, event count
+      const uint32_t nexp = hv2.x;
       kind = opw.x & 0xFFu;
       const uint32_t a = (opw.x >> 8) & 0xFFu;
       heavy = true;
@@ -1677,12 +1679,19 @@ __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_c
       s_cnt[threadIdx.x] = 0;
     }
     __syncthreads();
-    if (heavy) p.perm[(size_t)bk * p.num_traces + s_base[bk] + off + __popc(grp & lanemask_lt())] = t;
+    if (heavy) {  // the 64-B ticket: op, header words 0..11 (word 10 <- the trace id)
+      uint4* tk = reinterpret_cast<uint4*>(p.perm) +
+                  4 * ((size_t)bk * p.num_traces + s_base[bk] + off + __popc(grp & lanemask_lt()));
+      tk[0] = opw;
+      tk[1] = hv0;
+      tk[2] = hv1;
+      tk[3] = make_uint4(hv2.x, hv2.y, t, 0u);
+    }
   }
 }
 
 // bucketed item i of this step -> its trace (false past the heavy count)
-__device__ __forceinline__ bool item_trace(const StepArgs& args, uint32_t i, uint32_t& t) {
+__device__ __forceinline__ bool item_trace(const StepArgs& args, uint32_t i, const uint32_t*& tk) {
   const uint4* cnt4 = reinterpret_cast<const uint4*>(args.p.bcnt + (args.step & 1u) * 8);
   // read-only in this kernel and written by the previous one: the L1 path
   // serves every CTA of an SM after the first (an L2 round trip each before)
@@ -1696,12 +1705,12 @@ __device__ __forceinline__ bool item_trace(const StepArgs& args, uint32_t i, uin
     acc += c;
   }
   if (bk == 8) return false;
-  t = __ldg(args.p.perm + (size_t)bk * args.p.num_traces + off);
+  tk = args.p.perm + ((size_t)bk * args.p.num_traces + off) * 16;
   return true;
 }
 
-// one heavy trace-step of trace t: the warp's whole op path
-__device__ __forceinline__ void run_item(const StepArgs& args, uint32_t t) {
+// one heavy trace-step from its ticket: the warp's whole op path
+__device__ __forceinline__ void run_item(const StepArgs& args, const uint32_t* tk) {
   const uint32_t lane = threadIdx.x & 31u;
 #if RKC_BIG
   if (threadIdx.x >= 32) {  // crew helpers: block-pass slices until the leader is done
@@ -1710,11 +1719,18 @@ __device__ __forceinline__ void run_item(const StepArgs& args, uint32_t t) {
   }
 #endif
   const PoolDev& p = args.p;
-  const uint4 opw = __ldcs(args.ops + t);
+  // the ticket (written by the light pass, read through L1): lane l < 16 holds
+  // word l -- the op in words 0..3, header words 0..11 in 4..15, the trace id
+  // in place of (unused) header word 10
+  const uint32_t tw = lane < 16 ? __ldg(tk + lane) : 0u;
+  const uint4 opw = make_uint4(__shfl_sync(kFull, tw, 0), __shfl_sync(kFull, tw, 1),
+                               __shfl_sync(kFull, tw, 2), __shfl_sync(kFull, tw, 3));
+  const uint32_t t = __shfl_sync(kFull, tw, 14);
+  const uint32_t hsh = __shfl_sync(kFull, tw, (lane + 4) & 31u);
+  const uint32_t hw = lane < 10 ? hsh : 0u;  // hot header words 0..9 (10..15 unused)
   const uint32_t kind = opw.x & 0xFFu, a = (opw.x >> 8) & 0xFFu;
   // Issue every load this op is known to need before waiting on any of them:
   // hot header (lanes 0..15), the request record, the claim / object tables.
-  const uint32_t hw = lane < H_NWORDS ? __ldcg(p.hdr + (size_t)t * H_NWORDS + lane) : 0u;
   const bool rq_op = (kind == OP_ADMIT || kind == OP_ADVANCE || kind == OP_COMPLETE) && a < p.Q;
   const bool want_cl = kind == OP_SUBMIT || kind == OP_DEMOTE || kind == OP_TOUCH ||
                        kind == OP_COMPLETE || kind == OP_INSERT;
@@ -1803,9 +1819,9 @@ __device__ __forceinline__ void run_item(const StepArgs& args, uint32_t t) {
 __global__ void __launch_bounds__(kWarpsPerCta * kCrew * 32, 32 / (kWarpsPerCta * kCrew))
 rkc_step_kernel(const __grid_constant__ StepArgs args) {
   pdl_wait();
-  uint32_t t;
-  if (!item_trace(args, blockIdx.x * kWarpsPerCta + (kWarpsPerCta == 1 ? 0u : (threadIdx.x >> 5)), t)) return;
-  run_item(args, t);
+  const uint32_t* tk;
+  if (!item_trace(args, blockIdx.x * kWarpsPerCta + (kWarpsPerCta == 1 ? 0u : (threadIdx.x >> 5)), tk)) return;
+  run_item(args, tk);
 }
 
 #if !RKC_BIG
@@ -1824,9 +1840,9 @@ __host__ __device__ constexpr uint32_t kOverflowCtas(uint32_t T) {
 __global__ void __launch_bounds__(32) rkc_step_overflow_kernel(const __grid_constant__ StepArgs args) {
   pdl_wait();
   for (uint32_t i = kMainItems(args.p.num_traces) + blockIdx.x;; i += gridDim.x) {
-    uint32_t t;
-    if (!item_trace(args, i, t)) return;
-    run_item(args, t);
+    const uint32_t* tk;
+    if (!item_trace(args, i, tk)) return;
+    run_item(args, tk);
     __syncwarp();
   }
 }
