@@ -41,6 +41,11 @@ WORKLOADS = {
                desc="c4: 10k random traces per GPU, 65536-block pools (Llama-3-8B-sized KV), "
                     "T=1024 lockstep steps, long shared prefixes, demotion/expiry churn",
                l2="inputs larger than L2: pool state 5.2 GB + ops 0.16 GB per GPU, no flush"),
+    # c5 (configs[4]): 10^6 c3 traces in total, sharded over the ranks (strong scaling)
+    "c5": dict(recipe=3, traces=1_000_000, nblk=1024, steps=256, C=16, Q=16, O=64, ept=512, strong=True,
+               desc="c5: 10^6 random c3 traces sharded over the GPUs (1024-block pools, T=256 lockstep "
+                    "steps), outcome histograms NCCL-allreduced",
+               l2="inputs larger than L2: pool state 8.3 GB + ops 4.1 GB per GPU at N=1, no flush"),
 }
 WL = WORKLOADS["c3"]
 TRACES, NBLK, TSTEPS, C, Q, O, EPT = (WL[k] for k in ("traces", "nblk", "steps", "C", "Q", "O", "ept"))
@@ -52,9 +57,25 @@ def select_workload(name: str):
     TRACES, NBLK, TSTEPS, C, Q, O, EPT = (WL[k] for k in ("traces", "nblk", "steps", "C", "Q", "O", "ept"))
 
 
+def shard(rank: int, world: int) -> tuple[int, int]:
+    """(first trace id, trace count) of this rank: weak scaling replays TRACES
+    per rank; strong scaling (c5) splits WL["traces"] over the ranks."""
+    if not WL.get("strong"):
+        return rank * TRACES, TRACES
+    total = WL["traces"]
+    lo, hi = total * rank // world, total * (rank + 1) // world
+    return lo, hi - lo
+
+
+def scaling() -> str:
+    return "strong" if WL.get("strong") else "weak"
+
+
 def workload_config(n_gpus: int) -> dict:
-    return {"workload": WL["desc"], "traces_per_gpu": TRACES, "pool_blocks": NBLK,
-            "steps_per_replay": TSTEPS, "global_traces": TRACES * n_gpus,
+    per = shard(0, n_gpus)[1]
+    return {"workload": WL["desc"], "traces_per_gpu": per, "pool_blocks": NBLK,
+            "steps_per_replay": TSTEPS,
+            "global_traces": WL["traces"] if WL.get("strong") else TRACES * n_gpus,
             "parallelism": f"trace-sharded x{n_gpus}", "l2": WL["l2"]}
 
 
@@ -220,7 +241,7 @@ def run_reference(args, rank: int, world: int):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "higher_is_better": True, "scaling": scaling(), "vs_baseline": None, "dtype": "u32",
         "data": "synthetic", "config": workload_config(world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "oracle",
                          "sample": desc},
@@ -271,7 +292,9 @@ def main():
     local_rank = gpu
 
     # ---- inputs: this rank's shard, generated on the host, resident in HBM ----
-    cfgs, ops = gen.random_traces(WL["recipe"], SEED, rank * TRACES, TRACES, TSTEPS, NBLK, C, Q, O)
+    global TRACES
+    first, TRACES = shard(rank, world)
+    cfgs, ops = gen.random_traces(WL["recipe"], SEED, first, TRACES, TSTEPS, NBLK, C, Q, O)
     non_nop = int((ops["kind"] != 0).sum())
     ops_u8 = ops.view(np.uint8).reshape(-1)
     ops_dev = torch.from_numpy(ops_u8).to(dev)
@@ -369,7 +392,7 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "scaling": scaling(), "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": workload_config(world),
         "traces_per_s": total_traces * args.steps / (ms * 1e-3),
         "events_per_step": total_events,

@@ -1,0 +1,58 @@
+"""Bit-exact parity of the CUDA path with the oracle on 10^6 random c3 traces
+(BASELINE.json north_star: "bit-exact agreement with the CPU oracle across the
+full litmus suite and 10^6 random traces").  Test infrastructure, run by hand
+on a GPU box (about 10 minutes with 16 host threads), not collected by pytest:
+
+    python tests/run_parity_1m.py [--traces 1000000] [--chunk 20000] [--steps 256]
+
+Trace ids [0, traces) of the c3 recipe are replayed chunk by chunk (traces are
+independent): the GPU pool through the C ABI, the oracle on the host
+cores; per chunk every counter, every event record (in (trace, step, seq)
+order) and the full final state (header, blocks, claims, requests, objects)
+must be equal byte for byte.  Prints one line per chunk and a JSON summary.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+sys.path.insert(0, HERE)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--traces", type=int, default=1_000_000)
+    ap.add_argument("--chunk", type=int, default=20_000)
+    ap.add_argument("--steps", type=int, default=256)
+    ap.add_argument("--blocks", type=int, default=1024)
+    a = ap.parse_args()
+    import torch
+    from paper_2605_24259_b200 import gen
+    from parity_util import assert_parity, run_gpu, run_ref
+    threads = os.cpu_count() or 1
+    t0 = time.time()
+    n_ev = n_ops = 0
+    for begin in range(0, a.traces, a.chunk):
+        n = min(a.chunk, a.traces - begin)
+        cfgs, ops = gen.random_traces(3, seed=0, trace_begin=begin, n_traces=n, T=a.steps, N=a.blocks)
+        g = run_gpu(cfgs, ops, N=a.blocks, ept=512)
+        o = run_ref(cfgs, ops, N=a.blocks, nthreads=threads)
+        assert_parity(g, o, views=True, what=f"traces [{begin}, {begin + n})")
+        n_ev += len(g["events"])
+        n_ops += int((ops["kind"] != 0).sum())
+        del g, o
+        torch.cuda.empty_cache()
+        print(f"traces [{begin:7d}, {begin + n:7d}) bit-exact: counters, {n_ev} events so far, "
+              f"final state ({time.time() - t0:.0f} s)", flush=True)
+    print(json.dumps({"traces": a.traces, "steps": a.steps, "pool_blocks": a.blocks,
+                      "non_nop_ops": n_ops, "events": n_ev, "result": "bit-exact",
+                      "host_threads": threads, "seconds": round(time.time() - t0, 1)}))
+
+
+if __name__ == "__main__":
+    main()
