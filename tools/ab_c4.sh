@@ -3,6 +3,6 @@
 OUT=gpurun_out; mkdir -p $OUT
 : > $OUT/ab_c4.txt
 for lib in exp_libs/*.so; do
-  RKC_LIB=$lib timeout 300 python tools/step_timing.py --config 4 --traces 10000 --blocks 65536 --steps 64 --reps 2 --tag $(basename $lib .so) >> $OUT/ab_c4.txt 2>&1
+  RKC_LIB=$lib timeout 300 python tools/step_timing.py --config 4 --traces 10000 --blocks 65536 --steps ${C4_STEPS:-64} --reps 2 --tag $(basename $lib .so) >> $OUT/ab_c4.txt 2>&1
 done
 cat $OUT/ab_c4.txt
