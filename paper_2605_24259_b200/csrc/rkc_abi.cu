@@ -74,19 +74,34 @@ namespace {
 
 constexpr uint32_t kThreads = 256;
 
+// pool reset: block words four at a time (NS is a multiple of 128), 32-bit
+// index math while the word count fits
 __global__ void init_blocks_kernel(PoolDev p, const uint32_t* tcfg) {
-  const size_t total = (size_t)p.num_traces * p.NS;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+  const size_t total4 = (size_t)p.num_traces * (p.NS / 4);
+  const uint32_t ns4 = p.NS / 4;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total4;
        i += (size_t)gridDim.x * blockDim.x) {
-    const uint32_t t = (uint32_t)(i / p.NS), b = (uint32_t)(i % p.NS);
+    const uint32_t t = total4 < (1ull << 32) ? (uint32_t)i / ns4 : (uint32_t)(i / ns4);
+    const uint32_t b = (uint32_t)(i - (size_t)t * ns4) * 4;
     const uint32_t U = tcfg[t * 3];
-    p.key[i] = b < U ? b : kKeyActive;
-    p.meta[i] = b < U ? meta_make(kResFree, 0, 0) : meta_make(kResPad, 0, 0);
+    uint4 k, m;
+    k.x = b < U ? b : kKeyActive;
+    k.y = b + 1 < U ? b + 1 : kKeyActive;
+    k.z = b + 2 < U ? b + 2 : kKeyActive;
+    k.w = b + 3 < U ? b + 3 : kKeyActive;
+    const uint32_t mf = meta_make(kResFree, 0, 0), mp = meta_make(kResPad, 0, 0);
+    m.x = b < U ? mf : mp;
+    m.y = b + 1 < U ? mf : mp;
+    m.z = b + 2 < U ? mf : mp;
+    m.w = b + 3 < U ? mf : mp;
+    reinterpret_cast<uint4*>(p.key)[i] = k;
+    reinterpret_cast<uint4*>(p.meta)[i] = m;
   }
   const size_t nw = (size_t)p.num_traces * (p.NS / 32);
+  const uint32_t ns32 = p.NS / 32;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nw;
        i += (size_t)gridDim.x * blockDim.x) {
-    const uint32_t t = (uint32_t)(i / (p.NS / 32)), w = (uint32_t)(i % (p.NS / 32));
+    const uint32_t t = (uint32_t)(i / ns32), w = (uint32_t)(i % ns32);
     const uint32_t U = tcfg[t * 3];
     const uint32_t lo = w * 32;
     uint32_t word = 0;
@@ -96,24 +111,22 @@ __global__ void init_blocks_kernel(PoolDev p, const uint32_t* tcfg) {
   }
 }
 
+// headers (one thread per trace) and object records (element-parallel); the
+// claim / request / counter tables are cleared by memsets in run_init
 __global__ void init_tables_kernel(PoolDev p, const uint32_t* tcfg) {
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < p.num_traces;
        t += gridDim.x * blockDim.x) {
-    uint32_t* h = p.hdr + (size_t)t * H_NWORDS;
-    for (int i = 0; i < (int)H_NWORDS; ++i) h[i] = 0;
-    h[H_U] = tcfg[t * 3];
-    h[H_POLICY] = tcfg[t * 3 + 1];
-    h[H_ACCEPT] = tcfg[t * 3 + 2] & 0xFFu;
-    h[H_FREE] = tcfg[t * 3];
-    h[H_NEXT_EXPIRY] = 0xFFFFFFFFu;
-    for (uint32_t i = 0; i < p.C * 8; ++i) p.clm[(size_t)t * p.C * 8 + i] = 0;
-    for (uint32_t i = 0; i < p.Q * 8; ++i) p.req[(size_t)t * p.Q * 8 + i] = 0;
-    for (uint32_t o = 0; o < p.O; ++o) {
-      p.obj[((size_t)t * p.O + o) * 2] = obj_make(0, kNoClaim, 0);
-      p.obj[((size_t)t * p.O + o) * 2 + 1] = 0;
-    }
-    for (uint32_t k = 0; k < K_NCTR; ++k) p.ctr[(size_t)t * K_NCTR + k] = 0;
+    uint4* h = reinterpret_cast<uint4*>(p.hdr + (size_t)t * H_NWORDS);
+    const uint32_t U = tcfg[t * 3];
+    h[0] = make_uint4(U, tcfg[t * 3 + 1], tcfg[t * 3 + 2] & 0xFFu, 0u);   // U, policy, accept, seq
+    h[1] = make_uint4(U, 0u, 0u, 0u);                                     // free, alive, P, mask
+    h[2] = make_uint4(0xFFFFFFFFu, 0u, 0u, 0u);                           // next expiry, events
+    h[3] = make_uint4(0u, 0u, 0u, 0u);
   }
+  const size_t no = (size_t)p.num_traces * p.O;
+  const uint2 empty = make_uint2(obj_make(0, kNoClaim, 0), 0u);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < no; i += (size_t)gridDim.x * blockDim.x)
+    reinterpret_cast<uint2*>(p.obj)[i] = empty;
 }
 
 __global__ void stage_claim_kernel(const rkc_claim_input* in, uint32_t n, uint64_t identity,
@@ -249,8 +262,11 @@ rkc_status dev_alloc(rkc_pool* p, void** ptr, size_t bytes) {
 
 rkc_status run_init(rkc_pool* p, cudaStream_t st) {
   g_launches += 2;
-  init_blocks_kernel<<<grid_for((size_t)p->d.num_traces * p->d.NS), kThreads, 0, st>>>(p->d, p->tcfg);
-  init_tables_kernel<<<grid_for(p->d.num_traces), kThreads, 0, st>>>(p->d, p->tcfg);
+  init_blocks_kernel<<<grid_for((size_t)p->d.num_traces * p->d.NS / 4), kThreads, 0, st>>>(p->d, p->tcfg);
+  init_tables_kernel<<<grid_for((size_t)p->d.num_traces * p->d.O), kThreads, 0, st>>>(p->d, p->tcfg);
+  CUDA_TRY(cudaMemsetAsync(p->d.clm, 0, (size_t)p->d.num_traces * p->d.C * 32, st));
+  CUDA_TRY(cudaMemsetAsync(p->d.req, 0, (size_t)p->d.num_traces * p->d.Q * 32, st));
+  CUDA_TRY(cudaMemsetAsync(p->d.ctr, 0, (size_t)p->d.num_traces * K_NCTR * 4, st));
   CUDA_TRY(cudaMemsetAsync(p->staged, 0, sizeof(uint4) * p->d.num_traces, st));
   CUDA_TRY(cudaMemsetAsync(p->d.bcnt, 0, 16 * 4, st));
   CUDA_TRY(cudaMemsetAsync(p->owner_tag, 0xFF, sizeof(uint32_t) * p->d.num_traces, st));
