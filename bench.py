@@ -375,6 +375,19 @@ def main():
     if dist_on:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_ms = float(te[0])
+    # this box's pinned host->device copy bandwidth (the e2e floor is
+    # h2d_bytes_per_step / h2d_gbs when the copies outrun the steps)
+    probe = ops_pinned[: min(ops_pinned.numel(), 256 << 20)]
+    probe_dev = torch.empty(probe.numel(), dtype=torch.uint8, device=dev)
+    probe_dev.copy_(probe, non_blocking=True)
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h0.record(stream)
+    for _ in range(3):
+        probe_dev.copy_(probe, non_blocking=True)
+    h1.record(stream)
+    torch.cuda.synchronize()
+    h2d_gbs = 3 * probe.numel() / (h0.elapsed_time(h1) * 1e-3) / 1e9
+    del probe_dev
 
     # ---- telemetry of one replay for the algorithmic byte model (outside timing) ----
     counters, events, hist = pool.read_all()
@@ -412,6 +425,7 @@ def main():
                 "h2d_bytes_per_step": int(ops_u8.size),
                 "d2h_bytes_per_step": int(counters_host.nbytes + hist_host.nbytes),
                 "ms_per_step": e2e_ms,
+                "h2d_gbs_measured": h2d_gbs,
                 "path": "rkc_pool_reset + rkc_step_batch(pinned host ops) + "
                         "rkc_telemetry_read(host counters + histogram)"},
         "gpu_launches": int(launches),

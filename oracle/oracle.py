@@ -22,7 +22,8 @@ CLAIM_VIEW = np.dtype([("state", "u1"), ("mode", "u1"), ("obj", "u1"), ("pad", "
                        ("protected_blocks", "<u4")])
 REQUEST_VIEW = np.dtype([("status", "u1"), ("write_admit", "u1"), ("target", "u1"),
                          ("defer_count", "u1"), ("prompt", "<u4"), ("chunk", "<u4"),
-                         ("decode", "<u4"), ("done", "<u4"), ("live", "<u4"), ("pad", "<u4", (2,))])
+                         ("decode", "<u4"), ("done", "<u4"), ("live", "<u4"), ("hit", "<u4"),
+                         ("pad", "<u4")])
 OBJECT_VIEW = np.dtype([("live", "u1"), ("claim", "u1"), ("pad", "u1", (2,)), ("len", "<u4"),
                         ("leading", "<u4")])
 HEADER_VIEW = np.dtype([("seq_ctr", "<u4"), ("free_blocks", "<u4"), ("alive", "<u4"),
@@ -37,18 +38,20 @@ COUNTER_NAMES = [
     "deferred_capacity", "refused_protected", "refused_capacity", "inserted", "insert_refused",
     "write_denied", "victims_ordinary", "victims_after_release", "victims_claimed",
     "blocks_allocated", "blocks_cached", "reuse_probes", "reuse_tokens", "op_errors", "steps",
-    "events"]
+    "events", "prefix_hits", "hit_tokens"]
 K = {n: i for i, n in enumerate(COUNTER_NAMES)}
 
 # event types
 (E_CLAIM_ACCEPTED, E_CLAIM_REJECTED, E_CLAIM_MATERIALIZED, E_CLAIM_DEMOTED, E_CLAIM_EXPIRED,
  E_CLAIM_HARMED, E_ACTIVE_DEFERRED, E_ACTIVE_REFUSED, E_RESIDENT_INSERT_REFUSED,
- E_WRITE_ADMISSION_DENIED, E_REQUEST_SERVED, E_VICTIMS, E_REUSE_PROBE, E_OP_ERROR) = range(1, 15)
+ E_WRITE_ADMISSION_DENIED, E_REQUEST_SERVED, E_VICTIMS, E_REUSE_PROBE, E_OP_ERROR,
+ E_PREFIX_HIT) = range(1, 16)
 EVENT_NAMES = {1: "claim_accepted", 2: "claim_rejected", 3: "claim_materialized",
                4: "claim_demoted", 5: "claim_expired", 6: "claim_harmed",
                7: "active_request_deferred", 8: "active_request_refused",
                9: "resident_insert_refused", 10: "write_admission_denied",
-               11: "request_served", 12: "victims", 13: "reuse_probe", 14: "op_error"}
+               11: "request_served", 12: "victims", 13: "reuse_probe", 14: "op_error",
+               15: "prefix_hit"}
 # claim states / request status
 C_EMPTY, C_ACCEPTED, C_MATERIALIZED, C_DEMOTED, C_EXPIRED, C_REFUSED, C_HARMED = range(7)
 R_EMPTY, R_RUNNING, R_DEFERRED, R_REFUSED, R_COMPLETED = range(5)

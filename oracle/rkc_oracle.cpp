@@ -47,13 +47,13 @@ enum : uint8_t { M_SOFT = 0, M_HARD = 1, M_DEMOTABLE = 2, M_OFFLOADABLE = 3,
 enum : uint8_t { R_EMPTY = 0, R_RUNNING = 1, R_DEFERRED = 2, R_REFUSED = 3, R_COMPLETED = 4 };
 /* op kinds */
 enum : uint8_t { OP_NOP = 0, OP_SUBMIT = 1, OP_ADMIT = 2, OP_ADVANCE = 3, OP_COMPLETE = 4,
-                 OP_INSERT = 5, OP_DEMOTE = 6, OP_TOUCH = 7 };
+                 OP_INSERT = 5, OP_DEMOTE = 6, OP_TOUCH = 7, OP_HIT_ADMIT = 8 };
 /* event types (ClaimEvent; Table 4 required telemetry P:465-479) */
 enum : uint8_t { E_CLAIM_ACCEPTED = 1, E_CLAIM_REJECTED = 2, E_CLAIM_MATERIALIZED = 3,
                  E_CLAIM_DEMOTED = 4, E_CLAIM_EXPIRED = 5, E_CLAIM_HARMED = 6,
                  E_ACTIVE_DEFERRED = 7, E_ACTIVE_REFUSED = 8, E_RESIDENT_INSERT_REFUSED = 9,
                  E_WRITE_ADMISSION_DENIED = 10, E_REQUEST_SERVED = 11, E_VICTIMS = 12,
-                 E_REUSE_PROBE = 13, E_OP_ERROR = 14 };
+                 E_REUSE_PROBE = 13, E_OP_ERROR = 14, E_PREFIX_HIT = 15 };
 /* OP_ERROR codes */
 enum : uint8_t { ERR_DUPLICATE_SLOT = 1, ERR_INVALID_ARG = 2, ERR_ILLEGAL_TRANSITION = 3,
                  ERR_UNKNOWN_CLAIM = 4, ERR_UNKNOWN_REQUEST = 5, ERR_NO_CHUNKS_REMAINING = 6,
@@ -72,7 +72,7 @@ enum { K_OPS = 0, K_ACCEPTED, K_REJECTED, K_MATERIALIZED, K_DEMOTED_EXPLICIT, K_
        K_DEFERRED_PROTECTED, K_DEFERRED_CAPACITY, K_REFUSED_PROTECTED, K_REFUSED_CAPACITY,
        K_INSERTED, K_INSERT_REFUSED, K_WRITE_DENIED, K_VICTIMS_ORDINARY, K_VICTIMS_AFTER_RELEASE,
        K_VICTIMS_CLAIMED, K_BLOCKS_ALLOCATED, K_BLOCKS_CACHED, K_REUSE_PROBES, K_REUSE_TOKENS,
-       K_OP_ERRORS, K_STEPS, K_EVENTS, K_NCOUNTERS = 32 };
+       K_OP_ERRORS, K_STEPS, K_EVENTS, K_PREFIX_HITS, K_HIT_TOKENS, K_NCOUNTERS = 32 };
 
 const uint32_t BLOCK_TOKENS = 16;              /* P:615 "16-token block size" */
 const uint32_t NO_OBJ_CLAIM = 0xFF;            /* object has no claim binding */
@@ -90,7 +90,7 @@ struct BlockView { uint8_t res, owner; uint16_t pad; uint32_t pos, seq; };  /* 1
 struct ClaimView { uint8_t state, mode, obj, pad; uint32_t F, R, D, decision_step,
                    protected_blocks; };                                      /* 24 B */
 struct RequestView { uint8_t status, write_admit, target, defer_count;
-                     uint32_t prompt, chunk, decode, done, live, pad[2]; };  /* 32 B */
+                     uint32_t prompt, chunk, decode, done, live, hit, pad; };  /* 32 B */
 struct ObjectView { uint8_t live, claim, pad[2]; uint32_t len, leading; };  /* 12 B */
 struct HeaderView { uint32_t seq_ctr, free_blocks, alive, protected_total; }; /* 16 B */
 #pragma pack(pop)
@@ -106,8 +106,10 @@ struct Block { uint8_t res = B_FREE; uint8_t owner = 0; uint32_t pos = 0; uint32
 struct Object { bool live = false; uint32_t claim = NO_OBJ_CLAIM; uint32_t len = 0; };
 struct Claim { uint8_t state = C_EMPTY, mode = 0, obj = 0; uint32_t F = 0, R = 0, D = 0,
                decision_step = 0; };
+/* hit: leading blocks of the target object shared by a prefix hit (NEXT f3,
+ * G28); live counts only the request's own (exclusive) blocks. */
 struct Request { uint8_t status = R_EMPTY, write_admit = 0, target = 0, defer_count = 0;
-                 uint32_t prompt = 0, chunk = 0, decode = 0, done = 0, live = 0; };
+                 uint32_t prompt = 0, chunk = 0, decode = 0, done = 0, live = 0, hit = 0; };
 
 struct Dims { uint32_t N, C, Q, O; };
 
@@ -180,8 +182,24 @@ struct Trace {
    * exclusion"; BlockPool touch probe P:953-959), only under the
    * contract lowering (G6). */
   bool is_protected(uint32_t b) const {
-    if (cfg.lowering != LOW_CONTRACT || !claimed(b)) return false;
+    if (cfg.lowering != LOW_CONTRACT || !claimed(b) || pinned(b)) return false;
     return obligated(clm[claim_of_block(b)].mode);
+  }
+  /* pin_prefix(o): the longest prefix of object o shared by a running
+   * request's prefix hit (NEXT f3, "a leading-prefix hit", P:953
+   * BlockPool.touch; G28): the refcount of block (o, p) is the number of
+   * running requests with target o and hit > p. */
+  uint32_t pin_prefix(uint32_t o) const {
+    uint32_t m = 0;
+    for (const Request& r : req)
+      if (r.status == R_RUNNING && r.target == o && r.hit > m) m = r.hit;
+    return m;
+  }
+  /* pinned(b): a cached block some running request executes on (refcount
+   * > 0).  It is active live KV of that request, never a victim, and is
+   * counted in A, not in P (G29). */
+  bool pinned(uint32_t b) const {
+    return blk[b].res == B_CACHED && blk[b].pos < pin_prefix(blk[b].owner);
   }
   /* Allocation class (G1, G2, G6): 0 free (key block id), 1 ordinary cached
    * (key LRU stamp), 2 soft-priority cached (evicted after all class 1,
@@ -189,7 +207,7 @@ struct Trace {
   int alloc_class(uint32_t b) const {
     if (blk[b].res == B_FREE) return 0;
     if (blk[b].res == B_ACTIVE) return -1;
-    if (is_protected(b)) return -1;
+    if (pinned(b) || is_protected(b)) return -1;
     if (cfg.lowering != LOW_NATIVE && claimed(b)) {
       uint8_t m = clm[claim_of_block(b)].mode;
       if (m == M_SOFT || (cfg.lowering == LOW_SOFT && obligated(m))) return 2;
@@ -222,10 +240,13 @@ struct Trace {
       if (is_protected(b) && claim_of_block(b) == c) ++n;
     return n;
   }
-  /* Active live KV currently held: sum over running requests (G4). */
+  /* Active live KV currently held: sum over running requests (G4),
+   * plus every pinned cached block, counted once however many requests share
+   * it (G29). */
   uint32_t alive() const {
     uint32_t n = 0;
     for (const Request& r : req) if (r.status == R_RUNNING) n += r.live;
+    for (uint32_t b = 0; b < blk.size(); ++b) n += pinned(b) ? 1u : 0u;
     return n;
   }
   /* blocking_claim_ids: every claim with >= 1 protected block, ascending slot
@@ -248,6 +269,7 @@ struct Trace {
     for (Block& b : blk)
       if (b.res == B_ACTIVE && b.owner == r) { b.res = B_FREE; b.owner = 0; b.pos = 0; b.seq = 0; }
     req[r].live = 0;
+    req[r].hit = 0;  /* its prefix-hit references are dropped too (G28) */
   }
 
   /* -------------------------- arbiter (8c.4) ------------------------------ */
@@ -404,9 +426,54 @@ struct Trace {
     if (op.x < 1 || op.y < 1 || op.x > MAX_TOKENS || op.z > MAX_TOKENS) return op_error(op, ERR_INVALID_ARG);
     Request& q = req[r];
     q.status = R_RUNNING; q.write_admit = (uint8_t)wa; q.target = (uint8_t)target; q.defer_count = 0;
-    q.prompt = op.x; q.chunk = op.y; q.decode = op.z; q.done = 0; q.live = 0;
+    q.prompt = op.x; q.chunk = op.y; q.decode = op.z; q.done = 0; q.live = 0; q.hit = 0;
     ctr[K_ADMITTED]++;
     if (cfg.admit_check == ADMIT_PEAK) arbitrate(peak_blocks(q), (int)r, 0); /* G8 */
+  }
+
+  /* HIT_ADMIT (NEXT f3): admission of a request whose prompt begins with
+   * object o's content.  The hit is the leading surviving prefix, the
+   * materialization surface of P:303-304 and P:614-616 ("cached tokens equal
+   * the first missing block times the 16-token block size"), capped so that
+   * at least one prompt token is computed: h = min(leading(o),
+   * floor((prompt-1)/16)) (G28).  The hit blocks are shared, not allocated:
+   * the request starts at done = 16h, owns no block yet, and pins (o, 0..h-1)
+   * while it runs.  Pinning moves blocks into A (G29), so the PEAK check
+   * (G8) asks for the exclusive peak plus the newly pinned blocks that were
+   * candidates before: need = (peak - h) + |[m, h)| - |protected in [m, h)|,
+   * m = pin_prefix(o).  A hit refreshes the hit blocks' stamps tail-first,
+   * like TOUCH (G23, G30).  Hit requests do not write back (write_admit 0). */
+  void op_hit_admit(const OpRec& op) {
+    const uint32_t r = op.a, o = op.b;
+    if (r >= dims.Q || o >= dims.O || op.c != 0) return op_error(op, ERR_INVALID_ARG);
+    if (req[r].status == R_RUNNING || req[r].status == R_DEFERRED) return op_error(op, ERR_DUPLICATE_SLOT);
+    if (op.x < 1 || op.y < 1 || op.x > MAX_TOKENS || op.z > MAX_TOKENS) return op_error(op, ERR_INVALID_ARG);
+    const uint32_t L = leading(o);
+    const uint32_t h = std::min(L, (op.x - 1) / BLOCK_TOKENS);
+    if ((uint64_t)seq_ctr + h > SEQ_LIMIT) return op_error(op, ERR_SEQ_EXHAUSTED);
+    Request& q = req[r];
+    q.status = R_RUNNING; q.write_admit = 0; q.target = (uint8_t)o; q.defer_count = 0;
+    q.prompt = op.x; q.chunk = op.y; q.decode = op.z; q.done = 0; q.live = 0; q.hit = 0;
+    ctr[K_ADMITTED]++;
+    if (cfg.admit_check == ADMIT_PEAK) {
+      const uint32_t m = pin_prefix(o);
+      uint32_t newpin = 0, newprot = 0;
+      for (uint32_t b = 0; b < blk.size(); ++b) {
+        if (blk[b].res != B_CACHED || blk[b].owner != o || blk[b].pos < m || blk[b].pos >= h) continue;
+        newpin++;
+        if (is_protected(b)) newprot++;
+      }
+      if (!arbitrate(peak_blocks(q) - h + newpin - newprot, (int)r, 0)) return;
+    }
+    const uint32_t base = seq_ctr;
+    for (Block& b : blk)
+      if (b.res == B_CACHED && b.owner == o && b.pos < h) b.seq = base + (h - 1 - b.pos);
+    seq_ctr += h;
+    q.hit = h;
+    q.done = h * BLOCK_TOKENS;
+    emit(E_PREFIX_HIT, r, 0, 0, o, h, h * BLOCK_TOKENS, L);
+    ctr[K_PREFIX_HITS]++;
+    ctr[K_HIT_TOKENS] += h * BLOCK_TOKENS;
   }
 
   /* ADVANCE: one prefill chunk or one decode token (G14).  Live
@@ -427,7 +494,8 @@ struct Trace {
     if (q.done < q.prompt) n = std::min(q.chunk, q.prompt - q.done);
     else n = 1;
     const uint32_t need_total = (uint32_t)(((uint64_t)q.done + n + BLOCK_TOKENS - 1) / BLOCK_TOKENS);
-    const uint32_t need = need_total > q.live ? need_total - q.live : 0;
+    const uint32_t held = q.hit + q.live;  /* shared hit blocks + own blocks (G28) */
+    const uint32_t need = need_total > held ? need_total - held : 0;
     if (need > 0) {
       if (!arbitrate(need, (int)r, 0)) return;
       std::vector<uint32_t> taken = alloc(need, r, 0);
@@ -470,7 +538,7 @@ struct Trace {
     }
     emit(E_REQUEST_SERVED, r, admitted ? 1u : 0u, 0, q.done, admitted ? full : 0u, o);
     ctr[K_SERVED]++;
-    q.status = R_COMPLETED; q.live = 0;
+    q.status = R_COMPLETED; q.live = 0; q.hit = 0;
   }
 
   /* INSERT: resident insertion through the ordinary allocation path (G17). */
@@ -552,6 +620,7 @@ struct Trace {
       case OP_INSERT: op_insert(op); break;
       case OP_DEMOTE: op_demote(op); break;
       case OP_TOUCH: op_touch(op); break;
+      case OP_HIT_ADMIT: op_hit_admit(op); break;
       default: op_error(op, ERR_UNKNOWN_OP); break;
     }
     /* 3. post-op materialization predicate pass, ascending slot:
@@ -588,7 +657,12 @@ struct Trace {
     uint32_t held = 0;
     for (const Request& r : req) held += r.live;
     if (na != held) fail(1);
-    if (na != alive()) fail(1);
+    uint32_t npin = 0;
+    for (uint32_t b = 0; b < blk.size(); ++b) npin += pinned(b) ? 1u : 0u;
+    if (na + npin != alive()) fail(1);
+    /* I10 (f3): a pinned prefix is always fully present (never a victim) */
+    for (uint32_t o = 0; o < obj.size(); ++o)
+      if (pin_prefix(o) > leading(o)) fail(10);
     /* I2 (owner,pos) unique among non-free blocks; cached pos < len */
     std::vector<std::tuple<uint8_t, uint8_t, uint32_t>> ids;
     for (uint32_t i = 0; i < blk.size(); ++i) {
@@ -612,7 +686,7 @@ struct Trace {
       if (e.step == t && e.type == E_CLAIM_HARMED && e.reason == 1 && cfg.lowering == LOW_CONTRACT) fail(4);
     /* I9: running requests hold exactly ceil(done/16) blocks */
     for (const Request& r : req)
-      if (r.status == R_RUNNING && r.live != (r.done + BLOCK_TOKENS - 1) / BLOCK_TOKENS) fail(9);
+      if (r.status == R_RUNNING && r.hit + r.live != (r.done + BLOCK_TOKENS - 1) / BLOCK_TOKENS) fail(9);
   }
 };
 
@@ -732,7 +806,7 @@ void oracle_trace_export(void* h, uint32_t trace, void* hdr, void* blocks, void*
     const Request& q = tr.req[r];
     rv[r].status = q.status; rv[r].write_admit = q.write_admit; rv[r].target = q.target;
     rv[r].defer_count = q.defer_count; rv[r].prompt = q.prompt; rv[r].chunk = q.chunk;
-    rv[r].decode = q.decode; rv[r].done = q.done; rv[r].live = q.live;
+    rv[r].decode = q.decode; rv[r].done = q.done; rv[r].live = q.live; rv[r].hit = q.hit;
   }
   ObjectView* ov = (ObjectView*)objects;
   for (uint32_t o = 0; o < b->dims.O; ++o) {
@@ -767,7 +841,7 @@ void oracle_trace_import(void* h, uint32_t trace, uint32_t seq_ctr, uint32_t ste
     Request& q = tr.req[r];
     q.status = rv[r].status; q.write_admit = rv[r].write_admit; q.target = rv[r].target;
     q.defer_count = rv[r].defer_count; q.prompt = rv[r].prompt; q.chunk = rv[r].chunk;
-    q.decode = rv[r].decode; q.done = rv[r].done; q.live = rv[r].live;
+    q.decode = rv[r].decode; q.done = rv[r].done; q.live = rv[r].live; q.hit = rv[r].hit;
   }
   const ObjectView* ov = (const ObjectView*)objects;
   for (uint32_t o = 0; o < b->dims.O; ++o) {

@@ -25,7 +25,7 @@ CFG_DTYPE = np.dtype([("U", "<u4"), ("lowering", "u1"), ("admit_check", "u1"),
 assert OP_DTYPE.itemsize == 16 and CFG_DTYPE.itemsize == 12
 
 # op kinds
-NOP, SUBMIT, ADMIT, ADVANCE, COMPLETE, INSERT, DEMOTE, TOUCH = range(8)
+NOP, SUBMIT, ADMIT, ADVANCE, COMPLETE, INSERT, DEMOTE, TOUCH, HIT_ADMIT = range(9)
 # protection modes (Table 3)
 SOFT, HARD, DEMOTABLE, OFFLOADABLE, EXPIRING, BEST_EFFORT = range(6)
 # policy bytes
@@ -65,7 +65,7 @@ def _load():
 def random_traces(config: int, seed: int, trace_begin: int, n_traces: int, T: int,
                   N: int, C: int = 16, Q: int = 16, O: int = 64, nthreads: int | None = None,
                   ops_out: np.ndarray | None = None):
-    """Random traces of recipe `config` (3 = c3/c5, 4 = c4).
+    """Random traces of recipe `config` (3 = c3/c5, 4 = c4, 6 = c3 + prefix hits).
 
     Returns (cfgs[n_traces] CFG_DTYPE, ops[T, n_traces] OP_DTYPE).  ops_out
     may be a preallocated (e.g. pinned) uint8/OP_DTYPE buffer of T*n*16 bytes.

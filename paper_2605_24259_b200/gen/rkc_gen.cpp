@@ -37,7 +37,8 @@ struct Cfg { uint32_t U; uint8_t lowering, admit_check, defer_budget, auto_demot
 static_assert(sizeof(Op) == 16, "op");
 static_assert(sizeof(Cfg) == 12, "cfg");
 
-enum : uint8_t { NOP = 0, SUBMIT = 1, ADMIT = 2, ADVANCE = 3, COMPLETE = 4, INSERT = 5, DEMOTE = 6, TOUCH = 7 };
+enum : uint8_t { NOP = 0, SUBMIT = 1, ADMIT = 2, ADVANCE = 3, COMPLETE = 4, INSERT = 5, DEMOTE = 6, TOUCH = 7,
+                 HIT_ADMIT = 8 };
 
 inline uint64_t splitmix64(uint64_t& x) {
   uint64_t z = (x += 0x9E3779B97F4A7C15ull);
@@ -196,6 +197,17 @@ void gen_trace(int config, uint64_t seed, uint64_t trace_id, uint32_t T, uint32_
         if (config == 4) chunk = rc.chunks[g.uni(0, 2)];
         else { const uint32_t ch[4] = {128, 256, 512, 1024}; chunk = ch[g.uni(0, 3)]; }
         uint32_t decode = g.uni(0, rc.decode_hi);
+        if (config == 6 && !known_obj.empty() && g.bern(0.5)) {
+          /* c6 (NEXT f3): a prompt that begins with a known object's content
+           * -- a prefix hit on whatever of it survives -- plus new tokens */
+          const uint32_t ho = known_obj[g.uni(0, (uint32_t)known_obj.size() - 1)];
+          const uint32_t hp = 16 * g.uni(1, std::max<uint32_t>(1, obj_len[ho])) + g.uni(1, 2048);
+          op.kind = HIT_ADMIT; op.a = (uint8_t)r; op.b = (uint8_t)ho; op.c = 0;
+          op.x = hp; op.y = chunk; op.z = decode;
+          rq[r].active = true;
+          rq[r].remaining = (hp + chunk - 1) / chunk + decode;
+          break;
+        }
         uint8_t wa = g.bern(0.7) ? 1 : 0;
         int o = take_obj((prompt + decode) / 16);
         uint32_t target = o >= 0 ? (uint32_t)o : (known_obj.empty() ? 0 : known_obj[g.uni(0, (uint32_t)known_obj.size() - 1)]);
@@ -256,7 +268,7 @@ extern "C" {
 int rkc_gen_random(int config, uint64_t seed, uint64_t trace_begin, uint32_t n_traces, uint32_t T,
                    uint32_t N, uint32_t C, uint32_t Q, uint32_t O, void* cfg_out, void* ops_out,
                    int nthreads) {
-  if (config != 3 && config != 4) return -1;
+  if (config != 3 && config != 4 && config != 6) return -1;
   Cfg* cfgs = (Cfg*)cfg_out;
   Op* ops = (Op*)ops_out;
   std::atomic<uint32_t> next{0};

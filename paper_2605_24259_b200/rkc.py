@@ -39,7 +39,8 @@ CLAIM_VIEW = np.dtype([("state", "u1"), ("mode", "u1"), ("obj", "u1"), ("pad", "
                        ("protected_blocks", "<u4")])
 REQUEST_VIEW = np.dtype([("status", "u1"), ("write_admit", "u1"), ("target", "u1"),
                          ("defer_count", "u1"), ("prompt", "<u4"), ("chunk", "<u4"),
-                         ("decode", "<u4"), ("done", "<u4"), ("live", "<u4"), ("pad", "<u4", (2,))])
+                         ("decode", "<u4"), ("done", "<u4"), ("live", "<u4"), ("hit", "<u4"),
+                         ("pad", "<u4")])
 OBJECT_VIEW = np.dtype([("live", "u1"), ("claim", "u1"), ("pad", "u1", (2,)), ("len", "<u4"),
                         ("leading", "<u4")])
 HEADER_VIEW = np.dtype([("seq_ctr", "<u4"), ("free_blocks", "<u4"), ("alive", "<u4"),

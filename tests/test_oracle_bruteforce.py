@@ -6,7 +6,8 @@
    (class, key) vector is lexicographically smallest -- free blocks first
    (P:947-952), protected blocks never, then oldest stamp
    (G1), soft-priority last (G6).  Positions follow block-id order (G24).
-2. Exhaustive tiny traces: every op sequence of length 5 over a 12-op
+   Blocks pinned by a running prefix hit (f3, G28) are never candidates.
+2. Exhaustive tiny traces: every op sequence of length 5 over a 13-op
    alphabet on a 6-block pool, under two policies, runs with the oracle's
    debug invariants (I1-I9) on, and the event-level invariants I4-I7 hold.
 """
@@ -18,7 +19,7 @@ import pytest
 
 from oracle import oracle as orc
 from paper_2605_24259_b200.gen import (ADMIT, ADVANCE, COMPLETE, CONTRACT, DEMOTABLE, DEMOTE,
-                                       EXPIRING, HARD, INSERT, NATIVE, NONE, NOP, PEAK, SOFT,
+                                       EXPIRING, HARD, HIT_ADMIT, INSERT, NATIVE, NONE, NOP, PEAK, SOFT,
                                        SOFT_LOWERING, SUBMIT, TOUCH, BEST_EFFORT, make_cfg, op,
                                        pack_ops)
 
@@ -29,6 +30,12 @@ def _candidates(view, cfg):
     """(class, key) of every legal candidate block, from the state view."""
     blocks, claims, objs = view["blocks"], view["claims"], view["objects"]
     U = int(cfg["U"])
+    # pinned prefix per object: the longest running prefix hit on it (f3, G28)
+    pin = {}
+    for r in view["requests"]:
+        if int(r["status"]) == orc.R_RUNNING:
+            o = int(r["target"])
+            pin[o] = max(pin.get(o, 0), int(r["hit"]))
     out = {}
     for b in range(U):
         res = int(blocks[b]["res"])
@@ -38,6 +45,8 @@ def _candidates(view, cfg):
         if res == 2:
             continue
         o = int(blocks[b]["owner"])
+        if int(blocks[b]["pos"]) < pin.get(o, 0):
+            continue                                   # pinned by a running hit: never a victim
         c = int(objs[o]["claim"])
         claimed = (c != 0xFF and int(claims[c]["state"]) in (1, 2)
                    and int(blocks[b]["pos"]) < int(claims[c]["F"]))
@@ -65,7 +74,7 @@ def _random_tiny_ops(rng, U, T):
     ops = []
     for _ in range(T):
         k = rng.choice([INSERT, INSERT, SUBMIT, ADMIT, ADVANCE, ADVANCE, ADVANCE, COMPLETE,
-                        TOUCH, DEMOTE, NOP])
+                        TOUCH, DEMOTE, NOP, HIT_ADMIT])
         if k == INSERT:
             ops.append(op(INSERT, rng.randrange(4), x=rng.randint(1, U)))
         elif k == SUBMIT:
@@ -75,6 +84,9 @@ def _random_tiny_ops(rng, U, T):
                           F, rng.randint(1, F), rng.randint(1, 6)))
         elif k == ADMIT:
             ops.append(op(ADMIT, rng.randrange(2), rng.randrange(4), rng.randrange(2),
+                          rng.randint(1, 16 * U), rng.choice([16, 32, 48]), rng.randint(0, 20)))
+        elif k == HIT_ADMIT:
+            ops.append(op(HIT_ADMIT, rng.randrange(2), rng.randrange(4), 0,
                           rng.randint(1, 16 * U), rng.choice([16, 32, 48]), rng.randint(0, 20)))
         elif k in (ADVANCE, COMPLETE):
             ops.append(op(k, rng.randrange(2)))
@@ -140,6 +152,7 @@ ALPHABET = [
     op(SUBMIT, 1, 1, SOFT, 3, 2, 0), op(SUBMIT, 1, 1, DEMOTABLE, 3, 2, 2),
     op(ADMIT, 0, 2, 1, 48, 16, 2), op(ADMIT, 1, 3, 0, 64, 64, 0), op(ADVANCE, 0),
     op(ADVANCE, 1), op(COMPLETE, 0), op(DEMOTE, 0), op(TOUCH, 0),
+    op(HIT_ADMIT, 1, 1, 0, 40, 16, 1),                      # f3: hit on object 1's prefix
 ]
 
 

@@ -56,3 +56,17 @@ def test_random_c4_small_sample_invariants():
     b = orc.OracleBatch(cfgs, N=65536, C=16, Q=16, O=128)
     assert b.run(ops, nthreads=2, check=False) == 0
     assert b.counters().sum() > 0
+
+
+def test_random_c6_prefix_hit_invariants():
+    """c6 = c3 + prefix hits (NEXT f3): I1-I10 hold with pins in play (I10:
+    a pinned prefix is always fully present) and hits actually pin blocks."""
+    cfgs, ops = gen.random_traces(6, seed=7, trace_begin=0, n_traces=24, T=256, N=1024)
+    b = orc.OracleBatch(cfgs, N=1024)
+    assert b.run(ops, nthreads=8, check=True) == 0
+    ctr = b.counters().astype(np.int64).sum(0)
+    assert ctr[orc.K["prefix_hits"]] > 0 and ctr[orc.K["hit_tokens"]] > 0
+    per = b.counters()
+    for i in range(len(cfgs)):
+        if cfgs[i]["lowering"] == 0:
+            assert per[i][orc.K["harmed_obligated"]] == 0
