@@ -41,6 +41,12 @@ WORKLOADS = {
                desc="c4: 10k random traces per GPU, 65536-block pools (Llama-3-8B-sized KV), "
                     "T=1024 lockstep steps, long shared prefixes, demotion/expiry churn",
                l2="inputs larger than L2: pool state 5.2 GB + ops 0.16 GB per GPU, no flush"),
+    # c6 (NEXT f3): the c3 recipe with half of the admissions replaced by
+    # prefix-hit admissions on a known object (shared, pinned leading prefix)
+    "c6": dict(recipe=6, traces=100_000, nblk=1024, steps=256, C=16, Q=16, O=64, ept=512,
+               desc="c6: c3 + prefix hits (NEXT f3): 100k random traces per GPU, 1024-block pools, "
+                    "T=256 lockstep steps, half of the admissions share a known object's surviving prefix",
+               l2="inputs larger than L2: pool state 0.83 GB + ops 0.41 GB per GPU, no flush"),
     # c5 (configs[4]): 10^6 c3 traces in total, sharded over the ranks (strong scaling)
     "c5": dict(recipe=3, traces=1_000_000, nblk=1024, steps=256, C=16, Q=16, O=64, ept=512, strong=True,
                desc="c5: 10^6 random c3 traces sharded over the GPUs (1024-block pools, T=256 lockstep "
@@ -99,13 +105,16 @@ def algorithmic_bytes(ops: np.ndarray, counters: np.ndarray, events: np.ndarray)
     claim-state change   : reclass pass meta 4N + keys 4N (accepted, demoted, expired, harmed)
     INSERT               : object 8 + claim 32 + allocation as above + header write 64
     TOUCH                : object 8 + claim 32 + meta scan 4N + key read+write 8 per leading block
+    HIT_ADMIT (f3)       : request 32 read + 32 write + object table 8O + claim 32; a hit of
+                           h > 0 blocks: other requests' status/hit 8Q + meta scan 4N + 8 per
+                           pinned block + reclass pass 8N, and the same again when it unpins
     event                : 32 (write); counters 4 per op (reduction)
     """
     T, n = ops.shape
     kind = ops["kind"]
     N = NBLK
     et = events["type"]
-    cnt = {k: int((kind == k).sum()) for k in range(8)}
+    cnt = {k: int((kind == k).sum()) for k in range(9)}
     non_nop = n * T - cnt[0]
     vic = events[et == 12]
     n_evict = len(vic)
@@ -133,6 +142,10 @@ def algorithmic_bytes(ops: np.ndarray, counters: np.ndarray, events: np.ndarray)
     b += claim_changes * 8 * N
     b += cnt[5] * (8 + 32 + 64)
     b += touch_scans * 4 * N + cnt[7] * 40 + 8 * touch_blocks
+    hits = events[et == 15]
+    pinning = hits[hits["f"][:, 1] > 0]
+    b += cnt[8] * (64 + 8 * O + 32)
+    b += 2 * len(pinning) * (8 * Q + 4 * N + 8 * N) + 16 * int(pinning["f"][:, 1].astype(np.int64).sum())
     b += 32 * len(events) + 4 * non_nop
     return dict(bytes=int(b), non_nop=non_nop, evicting_selections=n_evict, events=len(events))
 

@@ -67,14 +67,22 @@ enum { RKC_REQ_EMPTY = 0, RKC_REQ_RUNNING = 1, RKC_REQ_DEFERRED = 2, RKC_REQ_REF
        RKC_REQ_COMPLETED = 4 };
 /* op kinds */
 enum { RKC_OP_NOP = 0, RKC_OP_SUBMIT = 1, RKC_OP_ADMIT = 2, RKC_OP_ADVANCE = 3,
-       RKC_OP_COMPLETE = 4, RKC_OP_INSERT = 5, RKC_OP_DEMOTE = 6, RKC_OP_TOUCH = 7 };
+       RKC_OP_COMPLETE = 4, RKC_OP_INSERT = 5, RKC_OP_DEMOTE = 6, RKC_OP_TOUCH = 7,
+       /* NEXT f3 (G28-G30): admission of a request whose
+        * prompt begins with object b's content.  a = request, b = object,
+        * c = 0, x/y/z = prompt/chunk/decode tokens.  The surviving leading
+        * prefix h = min(leading(b), (x-1)/16) is shared (pinned while the
+        * request runs: counted once in A, never a victim) instead of
+        * allocated; the request starts at 16h tokens and does not write back. */
+       RKC_OP_HIT_ADMIT = 8 };
 #define RKC_SUBMIT_ID_MISMATCH 0x80  /* flag in rkc_op.c of a SUBMIT */
 /* event types (ClaimEvent; Table 4 telemetry) */
 enum { RKC_EV_CLAIM_ACCEPTED = 1, RKC_EV_CLAIM_REJECTED = 2, RKC_EV_CLAIM_MATERIALIZED = 3,
        RKC_EV_CLAIM_DEMOTED = 4, RKC_EV_CLAIM_EXPIRED = 5, RKC_EV_CLAIM_HARMED = 6,
        RKC_EV_ACTIVE_DEFERRED = 7, RKC_EV_ACTIVE_REFUSED = 8, RKC_EV_RESIDENT_INSERT_REFUSED = 9,
        RKC_EV_WRITE_ADMISSION_DENIED = 10, RKC_EV_REQUEST_SERVED = 11, RKC_EV_VICTIMS = 12,
-       RKC_EV_REUSE_PROBE = 13, RKC_EV_OP_ERROR = 14 };
+       RKC_EV_REUSE_PROBE = 13, RKC_EV_OP_ERROR = 14,
+       RKC_EV_PREFIX_HIT = 15 /* slot = request; f = {object, h, 16h tokens, leading} */ };
 /* refusal reasons (G7) and OP_ERROR codes */
 enum { RKC_WHY_PROTECTED_RESIDENT = 1, RKC_WHY_ACTIVE_CAPACITY = 2 };
 enum { RKC_ERR_DUPLICATE_SLOT = 1, RKC_ERR_INVALID_ARG = 2, RKC_ERR_ILLEGAL_TRANSITION = 3,
@@ -93,7 +101,8 @@ enum { RKC_CTR_OPS = 0, RKC_CTR_ACCEPTED, RKC_CTR_REJECTED, RKC_CTR_MATERIALIZED
        RKC_CTR_REFUSED_CAPACITY, RKC_CTR_INSERTED, RKC_CTR_INSERT_REFUSED, RKC_CTR_WRITE_DENIED,
        RKC_CTR_VICTIMS_ORDINARY, RKC_CTR_VICTIMS_AFTER_RELEASE, RKC_CTR_VICTIMS_CLAIMED,
        RKC_CTR_BLOCKS_ALLOCATED, RKC_CTR_BLOCKS_CACHED, RKC_CTR_REUSE_PROBES,
-       RKC_CTR_REUSE_TOKENS, RKC_CTR_OP_ERRORS, RKC_CTR_STEPS, RKC_CTR_EVENTS };
+       RKC_CTR_REUSE_TOKENS, RKC_CTR_OP_ERRORS, RKC_CTR_STEPS, RKC_CTR_EVENTS,
+       RKC_CTR_PREFIX_HITS, RKC_CTR_HIT_TOKENS /* f3 */ };
 /* outcome histogram (int64[RKC_NHIST]):
  *   [0, 42)   final claim state (7) x mode (6): index state*6 + mode
  *   [42, 47)  final request status (5)
@@ -132,7 +141,8 @@ typedef struct { uint8_t res, owner; uint16_t pad; uint32_t pos, seq; } rkc_bloc
 typedef struct { uint8_t state, mode, obj, pad; uint32_t F, R, D, decision_step,
                  protected_blocks; } rkc_claim_view;
 typedef struct { uint8_t status, write_admit, target, defer_count;
-                 uint32_t prompt, chunk, decode, done, live, pad[2]; } rkc_request_view;
+                 uint32_t prompt, chunk, decode, done, live,
+                 hit /* shared prefix blocks (f3); live = own blocks */, pad; } rkc_request_view;
 typedef struct { uint8_t live, claim, pad[2]; uint32_t len, leading; } rkc_object_view;
 typedef struct { uint32_t seq_ctr, free_blocks, alive, protected_total; } rkc_header_view;
 #pragma pack(pop)

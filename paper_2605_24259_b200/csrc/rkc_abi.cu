@@ -660,7 +660,7 @@ rkc_status rkc_state_export(rkc_pool* pool, uint32_t trace_begin, uint32_t n,
         v.status = w[0] & 0xFF; v.write_admit = (w[0] >> 8) & 0xFF; v.target = (w[0] >> 16) & 0xFF;
         v.defer_count = w[0] >> 24;
         v.prompt = w[RQ_PROMPT]; v.chunk = w[RQ_CHUNK]; v.decode = w[RQ_DECODE];
-        v.done = w[RQ_DONE]; v.live = w[RQ_LIVE];
+        v.done = w[RQ_DONE]; v.live = w[RQ_LIVE]; v.hit = w[RQ_HIT];
       }
     }
     if (objects) {
@@ -699,8 +699,13 @@ rkc_status rkc_state_import(rkc_pool* pool, uint32_t trace_begin, uint32_t n,
     const rkc_claim_view* cv = claims + (size_t)i * d.C;
     const rkc_object_view* ov = objects + (size_t)i * d.O;
     const rkc_request_view* rv = requests + (size_t)i * d.Q;
-    std::vector<uint32_t> pc(d.C, 0), first_missing(d.O, 0xFFFFFFFFu);
+    std::vector<uint32_t> pc(d.C, 0), first_missing(d.O, 0xFFFFFFFFu), pin(d.O, 0);
     std::vector<std::vector<uint8_t>> present(d.O);
+    // pinned prefix per object: the longest hit of a running request (f3, G28)
+    for (uint32_t r = 0; r < d.Q; ++r)
+      if (rv[r].status == R_RUNNING && rv[r].target < d.O)
+        pin[rv[r].target] = std::max(pin[rv[r].target], rv[r].hit);
+    uint32_t npinned = 0;
     for (uint32_t o = 0; o < d.O; ++o) present[o].assign(ov[o].len, 0);
     uint32_t free_cnt = 0;
     for (uint32_t b = 0; b < NS; ++b) {
@@ -715,8 +720,15 @@ rkc_status rkc_state_import(rkc_pool* pool, uint32_t trace_begin, uint32_t n,
         meta[k] = meta_make(kResCached, v.owner, v.pos);
         uint32_t cls = 1;
         const uint32_t cc = ov[v.owner].claim;
-        if (cc < 32 && live_state_h(cv[cc].state) && v.pos < cv[cc].F) cls = claim_class_h(cv[cc].mode, low);
-        if (cls == 3) pc[cc]++;
+        const bool pinned = v.owner < d.O && v.pos < pin[v.owner];
+        if (pinned) {
+          meta[k] |= kMetaPin;
+          cls = 3;
+          ++npinned;
+        } else {
+          if (cc < 32 && live_state_h(cv[cc].state) && v.pos < cv[cc].F) cls = claim_class_h(cv[cc].mode, low);
+          if (cls == 3) pc[cc]++;
+        }
         key[k] = (cls << kClassShift) | (v.seq & kSeqMask);
         if (v.owner < d.O && v.pos < ov[v.owner].len) present[v.owner][v.pos] = 1;
       }
@@ -738,9 +750,10 @@ rkc_status rkc_state_import(rkc_pool* pool, uint32_t trace_begin, uint32_t n,
       uint32_t* w = &req[((size_t)i * d.Q + r) * 8];
       w[0] = rv[r].status | (rv[r].write_admit << 8) | (rv[r].target << 16) | (rv[r].defer_count << 24);
       w[RQ_PROMPT] = rv[r].prompt; w[RQ_CHUNK] = rv[r].chunk; w[RQ_DECODE] = rv[r].decode;
-      w[RQ_DONE] = rv[r].done; w[RQ_LIVE] = rv[r].live;
+      w[RQ_DONE] = rv[r].done; w[RQ_LIVE] = rv[r].live; w[RQ_HIT] = rv[r].hit;
       if (rv[r].status == R_RUNNING) alive += rv[r].live;
     }
+    alive += npinned;
     for (uint32_t o = 0; o < d.O; ++o) {
       uint32_t lead = ov[o].len;
       for (uint32_t q = 0; q < ov[o].len; ++q) if (!present[o][q]) { lead = q; break; }

@@ -537,11 +537,12 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
           const uint32_t o = meta_owner(m);
           if (!in_reclass(o)) continue;
           const uint32_t pos = meta_pos(m);
-          const uint32_t cls = pos < S.lim3[o] ? 3u : (pos < S.lim2[o] ? 2u : 1u);
+          const bool pin = meta_pinned(m);  // shared by a running hit: class 3, not protected (G29)
+          const uint32_t cls = (pin || pos < S.lim3[o]) ? 3u : (pos < S.lim2[o] ? 2u : 1u);
           const uint32_t k0 = el(kv, e);
           const uint32_t k1 = (cls << kClassShift) | (k0 & kSeqMask);
           if (k1 != k0) key[block_of(j, e)] = k1;
-          if (cls == 3) atomicAdd(&S.cnt3[o], 1u);
+          if (cls == 3 && !pin) atomicAdd(&S.cnt3[o], 1u);
         }
       }
       break;
@@ -679,11 +680,12 @@ __device__ __noinline__ void flush_reclass_pass() {
       const uint32_t o = meta_owner(m);
       if (!in_reclass(o)) continue;
       const uint32_t pos = meta_pos(m);
-      const uint32_t cls = pos < S.lim3[o] ? 3u : (pos < S.lim2[o] ? 2u : 1u);
+      const bool pin = meta_pinned(m);  // shared by a running hit: class 3, not protected (G29)
+      const uint32_t cls = (pin || pos < S.lim3[o]) ? 3u : (pos < S.lim2[o] ? 2u : 1u);
       const uint32_t k0 = el(kv, e);
       const uint32_t k1 = (cls << kClassShift) | (k0 & kSeqMask);
       if (k1 != k0) key[block_of(j, e)] = k1;
-      if (cls == 3) atomicAdd(&S.cnt3[o], 1u);
+      if (cls == 3 && !pin) atomicAdd(&S.cnt3[o], 1u);
     }
   };
 #if RKC_BIG
@@ -760,6 +762,73 @@ __device__ __forceinline__ void release_blocks(uint32_t r) {
   release_blocks_t<kBig>(r);
 }
 
+// ------------------------------ prefix hits (NEXT f3) ----------------------
+// pin_prefix(o): the longest hit on object o among running requests other
+// than `self` (their records are in HBM; the op's own one is in S.rq) -- the
+// refcount of block (o, p) is #{running r : target r = o, hit r > p} (G28)
+__device__ __noinline__ uint32_t pin_prefix(uint32_t o, uint32_t self) {
+  uint32_t h = 0;
+  if (lane_id() < S.Q && lane_id() != self) {
+    const uint32_t w0 = __ldcg(S.req + lane_id() * 8 + RQ_W0);
+    const uint32_t hq = __ldcg(S.req + lane_id() * 8 + RQ_HIT);
+    if ((w0 & 0xFFu) == R_RUNNING && ((w0 >> 16) & 0xFFu) == o) h = hq;
+  }
+  return __reduce_max_sync(kFull, h);
+}
+// pin (restamping tail-first, G30) or unpin the cached blocks (o, [lo, hi))
+template <bool big>
+__device__ __noinline__ void pin_pass_t(uint32_t o, uint32_t lo, uint32_t hi, bool pin,
+                                        uint32_t seq_base) {
+  uint32_t* key = S.key;
+  uint32_t* meta = S.meta;
+  const uint4* meta4 = reinterpret_cast<const uint4*>(meta);  // rare op: streamed, not staged
+  auto vec_pass = [&](uint32_t j) {
+    const uint4 mv = __ldcg(meta4 + j * 32 + lane_id());
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t m = el(mv, e);
+      if (meta_res(m) != kResCached || meta_owner(m) != o) continue;
+      const uint32_t pos = meta_pos(m);
+      if (pos < lo || pos >= hi) continue;
+      const uint32_t bb = block_of(j, e);
+      if (pin) {
+        meta[bb] = m | kMetaPin;
+        key[bb] = (3u << kClassShift) | (seq_base + (hi - 1 - pos));
+      } else {
+        meta[bb] = m & ~kMetaPin;  // class restored by the reclass pass
+      }
+    }
+  };
+  for_vec<big ? 4 : 1>(S.nv, vec_pass);
+  __syncwarp();
+}
+// request r (record in S.rq) drops its prefix-hit references: positions of
+// its target past the longest remaining hit are unpinned; A shrinks by them
+__device__ __noinline__ void unpin_request(uint32_t r) {
+  const uint32_t h = S.rq[RQ_HIT];
+  if (h == 0) return;
+  const uint32_t o = (S.rq[RQ_W0] >> 16) & 0xFFu;
+  const uint32_t m2 = pin_prefix(o, r);
+  __syncwarp();
+  if (lane_id() == 0) S.rq[RQ_HIT] = 0;
+  __syncwarp();
+  if (m2 >= h) return;
+  pin_pass_t<kBig>(o, m2, h, false, 0);
+  hset(H_ALIVE, S.h[H_ALIVE] - (h - m2));
+  mark_reclass(o);
+}
+// request r (record in S.rq) gives up all its KV: own blocks to FREE (A
+// shrinks by them) and its prefix-hit pins (deferral, refusal, no-admit
+// completion; G9, G28)
+__device__ __noinline__ void drop_request_kv(uint32_t r) {
+  const uint32_t live = S.rq[RQ_LIVE];
+  if (live > 0) {
+    release_blocks(r);
+    hset(H_ALIVE, S.h[H_ALIVE] - live);
+  }
+  unpin_request(r);
+}
+
 // ------------------------------ arbiter ------------------------------------
 // Feasibility boundary protected + active <= usable; relax by
 // auto-demotion (G10); else explicit refusal / deferral with
@@ -804,11 +873,7 @@ __device__ __noinline__ bool arbitrate(uint32_t need, uint32_t requester, uint32
     return false;
   }
   // request: release its live blocks, then defer or refuse (G9)
-  const uint32_t live = S.rq[RQ_LIVE];
-  if (live > 0) {
-    release_blocks(requester);
-    hset(H_ALIVE, S.h[H_ALIVE] - live);
-  }
+  drop_request_kv(requester);
   const uint32_t w0 = S.rq[RQ_W0];
   const uint32_t defer = w0 >> 24;
   const bool dfr = defer < ((pol >> 16) & 0xFFu);
@@ -1188,11 +1253,64 @@ __device__ __noinline__ void op_admit(const Op op) {
   if (lane_id() == 0) {
     S.rq[RQ_W0] = R_RUNNING | (op.c << 8) | (op.b << 16);
     S.rq[RQ_PROMPT] = op.x; S.rq[RQ_CHUNK] = op.y; S.rq[RQ_DECODE] = op.z;
-    S.rq[RQ_DONE] = 0; S.rq[RQ_LIVE] = 0;
+    S.rq[RQ_DONE] = 0; S.rq[RQ_LIVE] = 0; S.rq[RQ_HIT] = 0;
   }
   __syncwarp();
   ctr_add(K_ADMITTED, 1);
   if (((S.h[H_POLICY] >> 8) & 0xFFu) == ADMIT_PEAK) arbitrate(peak_blocks(), op.a, 0);
+  store_request(op.a);
+}
+
+// HIT_ADMIT (NEXT f3, G28-G30): admission through a prefix hit on
+// object b -- the surviving leading prefix, capped so
+// one prompt token is computed, is shared and pinned instead of allocated;
+// the PEAK check asks for the exclusive peak plus the newly pinned blocks
+// that were candidates (pinned blocks are active live KV, counted once).
+__device__ __noinline__ void op_hit_admit(const Op op) {
+  if (op.a >= S.Q || op.b >= S.O || op.c != 0) return op_error(op, ERR_INVALID_ARG);
+  load_request(op.a);
+  const uint32_t st = S.rq[RQ_W0] & 0xFFu;
+  if (st == R_RUNNING || st == R_DEFERRED) return op_error(op, ERR_DUPLICATE_SLOT);
+  if (op.x < 1 || op.y < 1 || op.x > kMaxTokens || op.z > kMaxTokens) return op_error(op, ERR_INVALID_ARG);
+  need_both();
+  const uint32_t o = op.b;
+  const uint32_t ow = S.obj0[o];
+  const uint32_t L = obj_live(ow) ? S.lead[o] : 0u;
+  const uint32_t h = min(L, (op.x - 1) / kBlockTokens);
+  if ((uint64_t)S.h[H_SEQ] + h > kSeqLimit) return op_error(op, ERR_SEQ_EXHAUSTED);
+  if (lane_id() == 0) {
+    S.rq[RQ_W0] = R_RUNNING | (o << 16);
+    S.rq[RQ_PROMPT] = op.x; S.rq[RQ_CHUNK] = op.y; S.rq[RQ_DECODE] = op.z;
+    S.rq[RQ_DONE] = 0; S.rq[RQ_LIVE] = 0; S.rq[RQ_HIT] = 0;
+  }
+  __syncwarp();
+  ctr_add(K_ADMITTED, 1);
+  const uint32_t m = h > 0 ? pin_prefix(o, op.a) : 0u;
+  const uint32_t newpin = h > m ? h - m : 0u;
+  if (((S.h[H_POLICY] >> 8) & 0xFFu) == ADMIT_PEAK) {
+    uint32_t newprot = 0;
+    const uint32_t cc = obj_claim(ow);
+    if (cc < 32 && live_state(cl_state(cc)) && claim_class(cl_mode(cc), lowering()) == 3) {
+      const uint32_t top = min(h, S.cl[cc][CF_F]);
+      newprot = top > m ? top - m : 0u;
+    }
+    if (!arbitrate(peak_blocks() - h + newpin - newprot, op.a, 0)) {
+      store_request(op.a);
+      return;
+    }
+  }
+  if (h > 0) {
+    const uint32_t seq_base = S.h[H_SEQ];
+    pin_pass_t<kBig>(o, 0, h, true, seq_base);
+    hset(H_SEQ, seq_base + h);
+    hset(H_ALIVE, S.h[H_ALIVE] + newpin);
+    mark_reclass(o);  // the claim's protected count loses the pinned positions
+  }
+  if (lane_id() == 0) { S.rq[RQ_HIT] = h; S.rq[RQ_DONE] = h * kBlockTokens; }
+  __syncwarp();
+  emit(EV_PREFIX_HIT, op.a, 0, 0, o, h, h * kBlockTokens, L);
+  ctr_add(K_PREFIX_HITS, 1);
+  ctr_add(K_HIT_TOKENS, h * kBlockTokens);
   store_request(op.a);
 }
 
@@ -1216,7 +1334,8 @@ __device__ __noinline__ void op_advance(const Op op) {
   const uint32_t done = S.rq[RQ_DONE], prompt = S.rq[RQ_PROMPT], live = S.rq[RQ_LIVE];
   const uint32_t n = done < prompt ? min(S.rq[RQ_CHUNK], prompt - done) : 1u;
   const uint32_t need_total = (uint32_t)(((uint64_t)done + n + kBlockTokens - 1) / kBlockTokens);
-  const uint32_t need = need_total > live ? need_total - live : 0u;
+  const uint32_t held = live + S.rq[RQ_HIT];  // own blocks + shared hit prefix (f3)
+  const uint32_t need = need_total > held ? need_total - held : 0u;
   if (need > 0) {
     if (!arbitrate(need, op.a, 0)) { store_request(op.a); return; }
     alloc(need, op.a, false, live);
@@ -1303,14 +1422,14 @@ __device__ __noinline__ void op_complete(const Op op) {
     add_protected(o, min(cls_lim3, full));
     ctr_add(K_BLOCKS_CACHED, full);
     flag_set(F_POST);
+    hset(H_ALIVE, S.h[H_ALIVE] - held);
   } else {
-    if (held > 0) release_blocks(op.a);
+    drop_request_kv(op.a);
     emit(EV_WRITE_DENIED, op.a, wa ? 1u : 0u, 0, o, held, 0, 0);
     ctr_add(K_WRITE_DENIED, 1);
   }
   emit(EV_SERVED, op.a, admitted ? 1u : 0u, 0, done, admitted ? full : 0u, o, 0);
   ctr_add(K_SERVED, 1);
-  hset(H_ALIVE, S.h[H_ALIVE] - held);
   if (lane_id() == 0) { S.rq[RQ_W0] = (S.rq[RQ_W0] & ~0xFFu) | R_COMPLETED; S.rq[RQ_LIVE] = 0; }
   __syncwarp();
   store_request(op.a);
@@ -1390,7 +1509,7 @@ __device__ __noinline__ void op_touch(const Op op) {
         const uint32_t m = el(mv, e);
         if (meta_res(m) == kResCached && meta_owner(m) == op.a && meta_pos(m) < L) {
           const uint32_t pos = meta_pos(m);
-          const uint32_t cls = pos < l3 ? 3u : (pos < l2 ? 2u : 1u);
+          const uint32_t cls = (meta_pinned(m) || pos < l3) ? 3u : (pos < l2 ? 2u : 1u);
           key[block_of(j, e)] = (cls << kClassShift) | (seq_base + (L - 1 - pos));
         }
       }
@@ -1521,6 +1640,7 @@ __device__ __forceinline__ uint32_t bucket_of(uint32_t kind) {
     case OP_TOUCH: return 3;
     case OP_SUBMIT: return 4;
     case OP_ADMIT: return 5;
+    case OP_HIT_ADMIT: return 5;
     case OP_DEMOTE: return 6;
     default: return 7;  // NOP and unknown kinds
   }
@@ -1572,14 +1692,14 @@ __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_c
         // level 2: the request record and (speculatively) the free bitmap
         uint32_t* rq = p.req + ((size_t)t * p.Q + a) * 8;
         const uint4 r0 = __ldcg(reinterpret_cast<const uint4*>(rq));
-        const uint2 r1 = __ldcg(reinterpret_cast<const uint2*>(rq + 4));
+        const uint4 r1 = __ldcg(reinterpret_cast<const uint4*>(rq + 4));
         const bool small = p.NS <= 1024;  // one bitmap word per lane
         const uint32_t status = r0.x & 0xFFu, prompt = r0.y, chunk = r0.z, decode = r0.w;
-        const uint32_t done = r1.x, live = r1.y;
+        const uint32_t done = r1.x, live = r1.y, held = r1.y + r1.z;  // own + shared hit blocks
         if (step < nexp && status == R_RUNNING && (uint64_t)done < (uint64_t)prompt + decode) {
           const uint32_t n = done < prompt ? min(chunk, prompt - done) : 1u;
           const uint64_t need_total = ((uint64_t)done + n + kBlockTokens - 1) / kBlockTokens;
-          if (need_total <= live) {
+          if (need_total <= held) {
             rq[RQ_DONE] = done + n;
             atomicAdd(p.ctr + (size_t)t * K_NCTR + K_OPS, 1u);
             heavy = false;
@@ -1587,7 +1707,7 @@ __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_c
             // a feasible allocation served entirely from free blocks: the
             // `need` lowest-id free blocks get positions live.. (G24); no
             // victim, no event, no claim or object change
-            const uint32_t need = (uint32_t)(need_total - live);
+            const uint32_t need = (uint32_t)(need_total - held);
             if ((uint64_t)hv1.z + hv1.y + need <= hv0.x && need <= hv1.x) {
               fa = true;  // the blocks are taken warp-cooperatively below
               fa_need = need;
@@ -1615,8 +1735,7 @@ __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_c
             reinterpret_cast<uint4*>(rq)[0] =
                 make_uint4(R_RUNNING | ((opw.x >> 24) << 8) | (((opw.x >> 16) & 0xFFu) << 16), opw.y,
                            opw.z, opw.w);
-            rq[RQ_DONE] = 0;
-            rq[RQ_LIVE] = 0;
+            reinterpret_cast<uint4*>(rq)[1] = make_uint4(0, 0, 0, 0);  // done, live, hit
             atomicAdd(p.ctr + (size_t)t * K_NCTR + K_OPS, 1u);
             atomicAdd(p.ctr + (size_t)t * K_NCTR + K_ADMITTED, 1u);
             heavy = false;
@@ -1731,10 +1850,12 @@ __device__ __forceinline__ void run_item(const StepArgs& args, const uint32_t* t
   const uint32_t kind = opw.x & 0xFFu, a = (opw.x >> 8) & 0xFFu;
   // Issue every load this op is known to need before waiting on any of them:
   // hot header (lanes 0..15), the request record, the claim / object tables.
-  const bool rq_op = (kind == OP_ADMIT || kind == OP_ADVANCE || kind == OP_COMPLETE) && a < p.Q;
+  const bool rq_op = (kind == OP_ADMIT || kind == OP_ADVANCE || kind == OP_COMPLETE ||
+                      kind == OP_HIT_ADMIT) && a < p.Q;
   const bool want_cl = kind == OP_SUBMIT || kind == OP_DEMOTE || kind == OP_TOUCH ||
-                       kind == OP_COMPLETE || kind == OP_INSERT;
-  const bool want_ob = kind == OP_SUBMIT || kind == OP_INSERT || kind == OP_COMPLETE || kind == OP_TOUCH;
+                       kind == OP_COMPLETE || kind == OP_INSERT || kind == OP_HIT_ADMIT;
+  const bool want_ob = kind == OP_SUBMIT || kind == OP_INSERT || kind == OP_COMPLETE ||
+                       kind == OP_TOUCH || kind == OP_HIT_ADMIT;
   uint32_t rqv = 0;
   if (rq_op && lane < 8) rqv = __ldcg(p.req + ((size_t)t * p.Q + a) * 8 + lane);
   uint4 c0 = make_uint4(0, 0, 0, 0), c1 = make_uint4(0, 0, 0, 0);
@@ -1805,6 +1926,7 @@ __device__ __forceinline__ void run_item(const StepArgs& args, const uint32_t* t
     case OP_INSERT: op_insert(op); break;
     case OP_DEMOTE: op_demote(op); break;
     case OP_TOUCH: op_touch<kBig>(op); break;
+    case OP_HIT_ADMIT: op_hit_admit(op); break;
     default: op_error(op, ERR_UNKNOWN_OP); break;
   }
   __syncwarp();
