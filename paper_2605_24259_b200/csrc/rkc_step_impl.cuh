@@ -775,10 +775,11 @@ __device__ __noinline__ uint32_t pin_prefix(uint32_t o, uint32_t self) {
   }
   return __reduce_max_sync(kFull, h);
 }
-// pin (restamping tail-first, G30) or unpin the cached blocks (o, [lo, hi))
+// pin (class 3, restamped tail-first, G30) or unpin (class from the bound
+// claim's limits l3 / l2, stamp kept) the cached blocks (o, [lo, hi))
 template <bool big>
 __device__ __noinline__ void pin_pass_t(uint32_t o, uint32_t lo, uint32_t hi, bool pin,
-                                        uint32_t seq_base) {
+                                        uint32_t seq_base, uint32_t l3, uint32_t l2) {
   uint32_t* key = S.key;
   uint32_t* meta = S.meta;
   const uint4* meta4 = reinterpret_cast<const uint4*>(meta);  // rare op: streamed, not staged
@@ -795,12 +796,36 @@ __device__ __noinline__ void pin_pass_t(uint32_t o, uint32_t lo, uint32_t hi, bo
         meta[bb] = m | kMetaPin;
         key[bb] = (3u << kClassShift) | (seq_base + (hi - 1 - pos));
       } else {
-        meta[bb] = m & ~kMetaPin;  // class restored by the reclass pass
+        meta[bb] = m & ~kMetaPin;
+        const uint32_t cls = pos < l3 ? 3u : (pos < l2 ? 2u : 1u);
+        key[bb] = (cls << kClassShift) | (__ldcg(key + bb) & kSeqMask);
       }
     }
   };
   for_vec<big ? 4 : 1>(S.nv, vec_pass);
   __syncwarp();
+}
+// the live claim bound to object o: its class-3 (protected) and class-2
+// (soft) footprint limits, 0 if none
+__device__ __forceinline__ void class_limits(uint32_t o, uint32_t& l3, uint32_t& l2) {
+  l3 = 0; l2 = 0;
+  const uint32_t cc = obj_claim(S.obj0[o]);
+  if (cc < 32 && live_state(cl_state(cc))) {
+    const uint32_t cls = claim_class(cl_mode(cc), lowering());
+    if (cls == 3) l3 = S.cl[cc][CF_F];
+    if (cls == 2) l2 = S.cl[cc][CF_F];
+  }
+}
+// the protected count of o's claim changes by d blocks (pins moved them in or out of P, G29)
+// (out of line: measured better for the instruction-cache footprint of both
+// the c3 and the c6 replay, profiles/r01/f3/README.md)
+__device__ __noinline__ void protected_delta(uint32_t o, int32_t d) {
+  if (d == 0) return;
+  const uint32_t cc = obj_claim(S.obj0[o]);
+  if (lane_id() == 0) S.cl[cc][CF_PC] += (uint32_t)d;
+  __syncwarp();
+  claims_dirty(lane_id() == cc);
+  refresh_protected();
 }
 // request r (record in S.rq) drops its prefix-hit references: positions of
 // its target past the longest remaining hit are unpinned; A shrinks by them
@@ -813,9 +838,13 @@ __device__ __noinline__ void unpin_request(uint32_t r) {
   if (lane_id() == 0) S.rq[RQ_HIT] = 0;
   __syncwarp();
   if (m2 >= h) return;
-  pin_pass_t<kBig>(o, m2, h, false, 0);
+  need_both();
+  uint32_t l3, l2;
+  class_limits(o, l3, l2);
+  pin_pass_t<kBig>(o, m2, h, false, 0, l3, l2);
   hset(H_ALIVE, S.h[H_ALIVE] - (h - m2));
-  mark_reclass(o);
+  const uint32_t top = min(h, l3);  // unpinned positions the claim protects again
+  protected_delta(o, top > m2 ? (int32_t)(top - m2) : 0);
 }
 // request r (record in S.rq) gives up all its KV: own blocks to FREE (A
 // shrinks by them) and its prefix-hit pins (deferral, refusal, no-admit
@@ -1288,12 +1317,10 @@ __device__ __noinline__ void op_hit_admit(const Op op) {
   const uint32_t m = h > 0 ? pin_prefix(o, op.a) : 0u;
   const uint32_t newpin = h > m ? h - m : 0u;
   if (((S.h[H_POLICY] >> 8) & 0xFFu) == ADMIT_PEAK) {
-    uint32_t newprot = 0;
-    const uint32_t cc = obj_claim(ow);
-    if (cc < 32 && live_state(cl_state(cc)) && claim_class(cl_mode(cc), lowering()) == 3) {
-      const uint32_t top = min(h, S.cl[cc][CF_F]);
-      newprot = top > m ? top - m : 0u;
-    }
+    uint32_t l3, l2;
+    class_limits(o, l3, l2);
+    const uint32_t top = min(h, l3);
+    const uint32_t newprot = top > m ? top - m : 0u;
     if (!arbitrate(peak_blocks() - h + newpin - newprot, op.a, 0)) {
       store_request(op.a);
       return;
@@ -1301,10 +1328,15 @@ __device__ __noinline__ void op_hit_admit(const Op op) {
   }
   if (h > 0) {
     const uint32_t seq_base = S.h[H_SEQ];
-    pin_pass_t<kBig>(o, 0, h, true, seq_base);
+    pin_pass_t<kBig>(o, 0, h, true, seq_base, 0, 0);
     hset(H_SEQ, seq_base + h);
     hset(H_ALIVE, S.h[H_ALIVE] + newpin);
-    mark_reclass(o);  // the claim's protected count loses the pinned positions
+    // the claim's protected count loses the newly pinned positions (the
+    // arbitration above may have demoted it: limits are read again)
+    uint32_t l3, l2;
+    class_limits(o, l3, l2);
+    const uint32_t top = min(h, l3);
+    protected_delta(o, top > m ? -(int32_t)(top - m) : 0);
   }
   if (lane_id() == 0) { S.rq[RQ_HIT] = h; S.rq[RQ_DONE] = h * kBlockTokens; }
   __syncwarp();

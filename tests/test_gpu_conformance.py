@@ -49,7 +49,8 @@ def test_pool_conformance_passes_on_gpu_streams():
     from paper_2605_24259_b200 import rkc
     for cfgs, ops, N in [litmus.paper_litmus()[:2] + (80,),
                          litmus.suite(range(200))[:2] + (1024,),
-                         gen.random_traces(3, 21, 0, 2000, 256, 1024) + (1024,)]:
+                         gen.random_traces(3, 21, 0, 2000, 256, 1024) + (1024,),
+                         gen.random_traces(6, 22, 0, 2000, 256, 1024) + (1024,)]:  # f3 hits
         pool = rkc.Pool(cfgs, N, events_per_trace=4 * ops.shape[0] + 64)
         pool.rkc_step_batch(torch.from_numpy(np.ascontiguousarray(ops).view(np.uint8).reshape(-1)).cuda(),
                             ops.shape[0])
