@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--chunk", type=int, default=20_000)
     ap.add_argument("--steps", type=int, default=256)
     ap.add_argument("--blocks", type=int, default=1024)
+    ap.add_argument("--config", type=int, default=3, help="generator recipe (3 = c3/c5, 6 = c6 hits)")
     a = ap.parse_args()
     import torch
     from paper_2605_24259_b200 import gen
@@ -39,7 +40,7 @@ def main():
     n_ev = n_ops = 0
     for begin in range(0, a.traces, a.chunk):
         n = min(a.chunk, a.traces - begin)
-        cfgs, ops = gen.random_traces(3, seed=0, trace_begin=begin, n_traces=n, T=a.steps, N=a.blocks)
+        cfgs, ops = gen.random_traces(a.config, seed=0, trace_begin=begin, n_traces=n, T=a.steps, N=a.blocks)
         g = run_gpu(cfgs, ops, N=a.blocks, ept=512)
         o = run_ref(cfgs, ops, N=a.blocks, nthreads=threads)
         assert_parity(g, o, views=True, what=f"traces [{begin}, {begin + n})")
@@ -49,7 +50,7 @@ def main():
         torch.cuda.empty_cache()
         print(f"traces [{begin:7d}, {begin + n:7d}) bit-exact: counters, {n_ev} events so far, "
               f"final state ({time.time() - t0:.0f} s)", flush=True)
-    print(json.dumps({"traces": a.traces, "steps": a.steps, "pool_blocks": a.blocks,
+    print(json.dumps({"config": a.config, "traces": a.traces, "steps": a.steps, "pool_blocks": a.blocks,
                       "non_nop_ops": n_ops, "events": n_ev, "result": "bit-exact",
                       "host_threads": threads, "seconds": round(time.time() - t0, 1)}))
 
