@@ -22,11 +22,12 @@ RKC_DECLARE_STEP(big_o128)
 #undef RKC_DECLARE_STEP
 std::atomic<unsigned long long> g_launches{0};  // kernels this library launched
 
-// one lockstep step = light pass + step kernel, from the build of the pool's
-// size class: <= 1024 blocks (keys staged in shared memory) or more, and
-// <= 64 object slots (32 resident CTAs per SM) or up to 128
+// one lockstep step = light pass + step kernel (+ the overflow kernel for
+// small pools), from the build of the pool's size class: <= 1024 blocks (keys
+// staged in shared memory) or more, and <= 64 object slots (32 resident CTAs
+// per SM) or up to 128
 static cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, cudaStream_t st) {
-  g_launches += 2;
+  g_launches += p.NS <= 1024 ? 3 : 2;
   if (p.NS <= 1024)
     return p.O <= 64 ? small_o64::launch_step(p, ops_step, step, st) : small_o128::launch_step(p, ops_step, step, st);
   return p.O <= 64 ? big_o64::launch_step(p, ops_step, step, st) : big_o128::launch_step(p, ops_step, step, st);
