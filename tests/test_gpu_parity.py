@@ -96,12 +96,14 @@ def test_host_replay_equals_device_replay():
     assert (g1["counters"] == g2["counters"]).all()
 
 
-def test_online_staging_api_equals_replay():
+@pytest.mark.parametrize("recipe", [3, 6])
+def test_online_staging_api_equals_replay(recipe):
     """rkc_claim_submit / rkc_request_admit / rkc_op_stage + rkc_step_batch(None)
-    give the same results as the replay of the same op stream."""
+    give the same results as the replay of the same op stream (recipe 6: the
+    prefix-hit admissions go through rkc_op_stage)."""
     from paper_2605_24259_b200 import rkc
     import torch
-    cfgs, ops = gen.random_traces(3, seed=6, trace_begin=0, n_traces=64, T=80, N=512)
+    cfgs, ops = gen.random_traces(recipe, seed=6, trace_begin=0, n_traces=64, T=80, N=512)
     ident = 0x1234
     pool = rkc.Pool(cfgs, 512, events_per_trace=512, pool_identity=ident)
     for s in range(ops.shape[0]):
