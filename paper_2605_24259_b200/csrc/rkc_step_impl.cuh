@@ -1252,6 +1252,7 @@ __device__ __noinline__ void op_submit(const Op op) {
     const uint32_t sum = __reduce_add_sync(kFull, lc ? S.cl[lane_id()][CF_F] : 0u);
     if ((uint64_t)op.x + sum > U) rej = REJ_RESERVE;
   }
+  __syncwarp();  // every lane has read the claim table (write-after-read in the warp)
   if (lane_id() == op.a) {
     uint32_t* r = S.cl[op.a];
     r[0] = (rej ? C_REFUSED : C_ACCEPTED) | (mode << 8) | (op.b << 16);
@@ -1279,6 +1280,7 @@ __device__ __noinline__ void op_admit(const Op op) {
   const uint32_t st = S.rq[RQ_W0] & 0xFFu;
   if (st == R_RUNNING || st == R_DEFERRED) return op_error(op, ERR_DUPLICATE_SLOT);
   if (op.x < 1 || op.y < 1 || op.x > kMaxTokens || op.z > kMaxTokens) return op_error(op, ERR_INVALID_ARG);
+  __syncwarp();  // every lane has read the request status (write-after-read in the warp)
   if (lane_id() == 0) {
     S.rq[RQ_W0] = R_RUNNING | (op.c << 8) | (op.b << 16);
     S.rq[RQ_PROMPT] = op.x; S.rq[RQ_CHUNK] = op.y; S.rq[RQ_DECODE] = op.z;
@@ -1307,6 +1309,7 @@ __device__ __noinline__ void op_hit_admit(const Op op) {
   const uint32_t L = obj_live(ow) ? S.lead[o] : 0u;
   const uint32_t h = min(L, (op.x - 1) / kBlockTokens);
   if ((uint64_t)S.h[H_SEQ] + h > kSeqLimit) return op_error(op, ERR_SEQ_EXHAUSTED);
+  __syncwarp();  // write-after-read in the warp
   if (lane_id() == 0) {
     S.rq[RQ_W0] = R_RUNNING | (o << 16);
     S.rq[RQ_PROMPT] = op.x; S.rq[RQ_CHUNK] = op.y; S.rq[RQ_DECODE] = op.z;
@@ -1360,6 +1363,7 @@ __device__ __noinline__ void op_advance(const Op op) {
       store_request(op.a);
       return;
     }
+    __syncwarp();  // write-after-read in the warp
     if (lane_id() == 0) S.rq[RQ_W0] = (S.rq[RQ_W0] & ~0xFFu) | R_RUNNING;
     __syncwarp();
   }
@@ -1374,6 +1378,7 @@ __device__ __noinline__ void op_advance(const Op op) {
     if (lane_id() == 0) S.rq[RQ_LIVE] = live + need;
     hset(H_ALIVE, S.h[H_ALIVE] + need);
   }
+  __syncwarp();  // write-after-read in the warp (no block needed: no sync since the reads)
   if (lane_id() == 0) S.rq[RQ_DONE] = done + n;
   __syncwarp();
   store_request(op.a);
@@ -1498,6 +1503,7 @@ __device__ __noinline__ void op_demote(const Op op) {
   if (st == C_EMPTY) return op_error(op, ERR_UNKNOWN_CLAIM);
   if (!live_state(st)) return op_error(op, ERR_ILLEGAL_TRANSITION);
   const uint32_t o = cl_obj(op.a), pc = S.cl[op.a][CF_PC], mode = cl_mode(op.a);
+  __syncwarp();  // write-after-read in the warp
   if (lane_id() == 0) { S.cl[op.a][0] = (S.cl[op.a][0] & ~0xFFu) | C_DEMOTED; S.cl[op.a][CF_PC] = 0; }
   __syncwarp();
   claims_dirty(lane_id() == op.a);
@@ -1629,6 +1635,7 @@ __device__ __noinline__ void finish() {
                             ? (uint32_t)min((uint64_t)r[CF_DEC] + r[CF_D], (uint64_t)0xFFFFFFFFu)
                             : 0xFFFFFFFFu;
     const uint32_t m = __reduce_min_sync(kFull, ne);
+    __syncwarp();  // write-after-read of S.flags in the warp
     if (lane_id() == 0) { S.h[H_NEXT_EXPIRY] = m; S.flags |= F_HDR; }
     __syncwarp();
   }
