@@ -195,14 +195,33 @@ def load_peak() -> tuple[float, str]:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic() -> float | None:
-    """dram bytes per lockstep step from the committed ncu --set full capture of this workload."""
+def _ncu_json() -> dict | None:
     name = "ncu_step_kernel.json" if WL is WORKLOADS["c3"] else f"ncu_step_kernel_{WL['desc'][:2]}.json"
-    p = os.path.join(ROOT, "profiles", name)
     try:
-        return float(json.load(open(p))["dram_bytes_per_launch"])
+        return json.load(open(os.path.join(ROOT, "profiles", name)))
     except Exception:
         return None
+
+
+def load_traffic() -> float | None:
+    """dram bytes per lockstep step from the committed ncu --set full capture of this workload."""
+    d = _ncu_json()
+    return float(d["dram_bytes_per_launch"]) if d and "dram_bytes_per_launch" in d else None
+
+
+def issue_roofline(step_us: float, sm_mhz: float) -> dict | None:
+    """Secondary roofline: the step is issue / latency bound, so report the
+    warp-instruction rate of one lockstep step (instructions per step from the committed ncu
+    capture, time from this run) against the issue peak 148 SMs x 4 schedulers x 1 warp
+    instruction per cycle at the SM clock measured during the timed region."""
+    d = _ncu_json()
+    if not d or "warp_instructions_per_launch" not in d or not sm_mhz:
+        return None
+    achieved = d["warp_instructions_per_launch"] / (step_us * 1e-6) / 1e12
+    peak = 148 * 4 * sm_mhz * 1e6 / 1e12
+    return {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "T warp-inst/s",
+            "frac": achieved / peak, "source": "warp instructions per step: profiles/" +
+            ("ncu_step_kernel.json" if WL is WORKLOADS["c3"] else f"ncu_step_kernel_{WL['desc'][:2]}.json")}
 
 
 # --------------------------------------------------------------------------
@@ -444,6 +463,9 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clk,
     }
+    iss = issue_roofline(per_launch_ms * 1e3, (clk or {}).get("sm_mhz") or 0)
+    if iss:
+        out["roofline_issue"] = iss
     if not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfgs, ops)
     print(json.dumps(out), flush=True)

@@ -28,9 +28,11 @@ def main(path, out, source):
         name = row[col["Kernel Name"]].split("(")[0].split("::")[-1]
         kernels[name] = {"dram_bytes_read": val(row, "dram__bytes_read.sum"),
                          "dram_bytes_write": val(row, "dram__bytes_write.sum"),
-                         "duration_us_cold": val(row, "gpu__time_duration.sum")}
+                         "duration_us_cold": val(row, "gpu__time_duration.sum"),
+                         "warp_instructions": val(row, "smsp__inst_executed.sum")}
     total = sum(k["dram_bytes_read"] + k["dram_bytes_write"] for k in kernels.values())
-    json.dump({"source": source, "kernels": kernels,
+    inst = sum(k["warp_instructions"] for k in kernels.values())
+    json.dump({"source": source, "kernels": kernels, "warp_instructions_per_launch": inst,
                "kernel": "one lockstep step = rkc_light_kernel + rkc_step_kernel + rkc_step_overflow_kernel",
                "dram_bytes_per_launch": total}, open(out, "w"), indent=1)
     print(json.dumps(kernels, indent=1), total)
