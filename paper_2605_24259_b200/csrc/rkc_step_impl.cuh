@@ -1090,15 +1090,31 @@ __device__ __noinline__ void alloc_evict(uint32_t k, uint32_t owner, bool insert
   bool bracket = false;
   uint32_t mult = 1;
   uint32_t T;
+  // big pools: every probe is a crew pass over the whole pool, so the search
+  // extrapolates the density seen so far (secant from the smallest key, 5/4
+  // overshoot to bracket) and interpolates first once bracketed; the result
+  // is the same set {key <= T} whatever the probe sequence (keys are unique)
+  const uint32_t lo0 = lo, clo0 = clo;
+  uint32_t bi = 0, last_d = 0;
   for (uint32_t it = 0;; ++it) {
     uint32_t m;
     if (!bracket) {
-      const uint64_t d = (uint64_t)(k - clo) * mult;
-      m = (uint32_t)min((uint64_t)lo + d, (uint64_t)top);
-      mult = mult < (1u << 20) ? mult * 4 : mult;
+      if (!staged && it > 0 && clo > clo0) {
+        // secant step, but never less than twice the last step (no creeping)
+        uint64_t d = ((uint64_t)(k - clo) * (lo - lo0) * 5) / ((uint64_t)(clo - clo0) * 4) + 1;
+        d = max(d, 2 * (uint64_t)last_d);
+        last_d = (uint32_t)min(d, (uint64_t)0xFFFFFFFFu);
+        m = (uint32_t)min((uint64_t)lo + d, (uint64_t)top);
+      } else {
+        const uint64_t d = (uint64_t)(k - clo) * mult;
+        m = (uint32_t)min((uint64_t)lo + d, (uint64_t)top);
+        mult = mult < (1u << 20) ? mult * 4 : mult;
+        last_d = (uint32_t)min(d, (uint64_t)0xFFFFFFFFu);
+      }
     } else {
       const uint32_t span = hi - lo;
-      m = (it & 1u) ? lo + (uint32_t)(((uint64_t)(k - clo) * span) / (chi - clo)) : lo + span / 2;
+      const bool interp = staged ? (it & 1u) != 0 : (bi++ & 1u) == 0;
+      m = interp ? lo + (uint32_t)(((uint64_t)(k - clo) * span) / (chi - clo)) : lo + span / 2;
       m = max(m, lo + 1);
       m = min(m, hi - 1);
     }
