@@ -44,6 +44,14 @@ def _litmus():
                        op(ADVANCE, 0), op(TOUCH, 0), op(HIT_ADMIT, 1, 0, 0, 16 * A + 3, 48, 5),
                        op(ADMIT, 2, 1, 1, 16 * (U // 2), 64, 0), op(ADVANCE, 2), op(COMPLETE, 0),
                        op(ADVANCE, 1), op(COMPLETE, 1), op(TOUCH, 0)])
+    from paper_2605_24259_b200.gen import DEMOTABLE
+    for _ in range(100):  # auto-demotion inside the hit's PEAK check, then the backstop (G29)
+        R = int(rng.integers(2, 80)); A = int(rng.integers(R + 1, 140))
+        U = int(rng.integers(A - R + 1, R + A + 5))
+        cfgs.append(make_cfg(U, CONTRACT, PEAK, defer_budget=int(rng.integers(0, 2)), auto_demote=1))
+        traces.append([op(INSERT, 0, x=R), op(SUBMIT, 0, 0, DEMOTABLE, R, R, 0),
+                       op(HIT_ADMIT, 0, 0, 0, 16 * A, 16 * A, 0), op(ADVANCE, 0), op(ADVANCE, 0),
+                       op(COMPLETE, 0), op(TOUCH, 0)])
     return np.stack(cfgs), pack_ops(traces)
 
 

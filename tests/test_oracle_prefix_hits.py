@@ -188,3 +188,28 @@ def test_hit_admit_errors():
                                                 orc.ERR_DUPLICATE_SLOT]
     hit = ev[ev["type"] == orc.E_PREFIX_HIT][0]
     assert list(hit["f"]) == [0, 0, 0, 0]
+
+
+def test_auto_demotion_during_hit_peak_check_then_backstop():
+    """G29's reading of a PEAK check that auto-demotes the hit object's own
+    claim: at HIT_ADMIT, P = 60, A = 0, need = (75-60)
+    + 60 - 60 = 15 -> 75 > 70, so the demotable claim is demoted (P' = 0 fits);
+    the 60 hit blocks are then pinned unprotected (A = 60).  The first chunk
+    needs 15 own blocks: 0 + 60 + 15 = 75 > 70 -> refused by the per-allocation
+    backstop with the capacity proof (0, 75, 70, 5), ACTIVE_CAPACITY (P = 0)."""
+    cfg = make_cfg(70, CONTRACT, PEAK, defer_budget=0, auto_demote=1)
+    from paper_2605_24259_b200.gen import DEMOTABLE
+    ops = [op(INSERT, 0, x=60), op(SUBMIT, 0, 0, DEMOTABLE, 60, 60, 0),
+           op(HIT_ADMIT, 0, 0, 0, 16 * 75, 16 * 75, 0), op(ADVANCE, 0)]
+    b = _run(cfg, ops, 70)
+    ev = b.events()
+    assert _types(ev) == ["claim_accepted", "claim_materialized", "claim_demoted", "prefix_hit",
+                          "active_request_refused"]
+    assert ev[2]["reason"] == 1 and list(ev[2]["f"][:2]) == [0, 60]     # auto, 60 protected released
+    assert list(ev[3]["f"]) == [0, 60, 960, 60]
+    ref = ev[4]
+    assert ref["reason"] == orc.WHY_ACTIVE_CAPACITY and ref["mask"] == 0
+    assert list(ref["f"]) == [0, 75, 70, 5]
+    st = b.export(0)
+    assert st["header"]["alive"] == 0 and st["requests"][0]["hit"] == 0   # pins dropped
+    assert st["claims"][0]["state"] == orc.C_DEMOTED
