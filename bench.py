@@ -383,8 +383,10 @@ def main():
     ms, step_kernel_ms = float(t[0]), float(t[1])
 
     # ---- e2e: the public C-ABI call with HOST buffers (pinned ops in, results out) ----
-    counters_host = np.zeros((TRACES, rkc.RKC_NCTR), dtype=np.uint32)
-    hist_host = np.zeros(rkc.RKC_NHIST, dtype=np.int64)
+    # results land in pinned host memory (a user's choice the C ABI allows)
+    counters_host = torch.zeros((TRACES, rkc.RKC_NCTR), dtype=torch.int32,
+                                pin_memory=True).numpy().view(np.uint32)
+    hist_host = torch.zeros(rkc.RKC_NHIST, dtype=torch.int64, pin_memory=True).numpy()
     # one untimed pass first: the library allocates its host-replay buffers on
     # first use and the pinned pages are touched once
     pool.rkc_pool_reset(stream)

@@ -517,8 +517,13 @@ rkc_status rkc_step_batch(rkc_pool* pool, const rkc_op* ops, uint32_t num_steps,
   CUDA_TRY(cudaEventRecord(pool->ev_free[1], st));
   uint32_t done = 0;
   int buf = 0;
+  // chunk sizes ramp up (2, 8, 32, ... steps) so the first steps wait for a
+  // small copy only; each later copy overlaps the previous chunk's steps
+  size_t ramp = 2;
   while (done < num_steps) {
-    const uint32_t n = (uint32_t)((num_steps - done) < chunk ? (num_steps - done) : chunk);
+    const size_t lim = ramp < chunk ? ramp : chunk;
+    ramp *= 4;
+    const uint32_t n = (uint32_t)((num_steps - done) < lim ? (num_steps - done) : lim);
     CUDA_TRY(cudaStreamWaitEvent(pool->copy_stream, pool->ev_free[buf], 0));
     CUDA_TRY(cudaMemcpyAsync(pool->replay_buf[buf], ops + (size_t)done * T, (size_t)n * T * 16,
                              cudaMemcpyHostToDevice, pool->copy_stream));
