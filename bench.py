@@ -2,14 +2,15 @@
 """bench.py -- batched resident-KV-claim arbitration on B200 (BASELINE.json metric:
 allocator events/s and traces/s at 1/2/4/8 GPUs, % of HBM roofline).
 
-One bench step = one pass of the whole hot path over one batch (DESIGN.md sec. 4):
-  rkc_pool_reset -> rkc_step_batch(T=256 lockstep steps over 100k traces, ops
+One bench step = one pass of the whole hot path over one batch (DESIGN.md sec. 6):
+  rkc_pool_reset -> rkc_step_batch(T=256 lockstep steps over this rank's traces, ops
   resident in HBM) -> rkc_telemetry_read (K2 event compaction + K3 outcome
   histogram, device outputs) -> NCCL allreduce of the histogram (N > 1).
-Workload (config c3, weak scaling): 100,000 random traces per GPU, 1024-block pools,
-T = 256 steps; rank r replays trace ids [r*100k, (r+1)*100k).
+Default workload (config c5 = BASELINE.json configs[4], strong scaling): 10^6 random
+traces in total, 1024-block pools, T = 256 steps; rank r of N replays trace ids
+[r*10^6/N, (r+1)*10^6/N).  --config c3 (100k traces per GPU, weak scaling), c4, c6.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config c3|c4|c5|c6]
 Under torchrun (N > 1) every rank runs; rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
@@ -30,8 +31,10 @@ sys.path.insert(0, ROOT)
 METRIC = "allocator events/sec and traces/sec at 1/2/4/8 B200; % of HBM roofline"
 UNIT = "events/s"
 SEED = 0
-# workloads: c3 is the bench default (BASELINE.json configs[2]);
-# c4 (configs[3]) is selectable with --config c4
+# workloads: the default is c5 (BASELINE.json configs[4], "1M random
+# traces sharded over 1/2/4/8 B200" -- the configuration the metric "at 1/2/4/8 B200" is
+# quoted on; it fits one GPU); c3 (configs[2], 100k traces per GPU, weak scaling), c4
+# (configs[3]) and c6 (c3 + prefix hits) are selectable with --config
 WORKLOADS = {
     "c3": dict(recipe=3, traces=100_000, nblk=1024, steps=256, C=16, Q=16, O=64, ept=512,
                desc="c3: 100k random traces per GPU, 1024-block pools (16-token blocks), T=256 "
@@ -55,6 +58,14 @@ WORKLOADS = {
 }
 WL = WORKLOADS["c3"]
 TRACES, NBLK, TSTEPS, C, Q, O, EPT = (WL[k] for k in ("traces", "nblk", "steps", "C", "Q", "O", "ept"))
+
+
+_T0 = time.time()
+
+
+def _phase(what: str) -> None:
+    """wall-clock progress on stderr (the JSON line stays alone on stdout)"""
+    print(f"[bench {time.time() - _T0:7.1f} s] {what}", file=sys.stderr, flush=True)
 
 
 def select_workload(name: str):
@@ -291,7 +302,7 @@ def main():
     ap.add_argument("--impl", default="rkc", choices=["rkc", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="c5", choices=sorted(WORKLOADS))
     args = ap.parse_args()
     select_workload(args.config)
     args.warmup = max(3, args.warmup)
@@ -326,12 +337,14 @@ def main():
     # ---- inputs: this rank's shard, generated on the host, resident in HBM ----
     global TRACES
     first, TRACES = shard(rank, world)
+    _phase("start")
     cfgs, ops = gen.random_traces(WL["recipe"], SEED, first, TRACES, TSTEPS, NBLK, C, Q, O)
     non_nop = int((ops["kind"] != 0).sum())
     ops_u8 = ops.view(np.uint8).reshape(-1)
     ops_dev = torch.from_numpy(ops_u8).to(dev)
     ops_pinned = torch.empty(ops_u8.size, dtype=torch.uint8, pin_memory=True)
     ops_pinned.numpy()[:] = ops_u8
+    _phase("inputs generated and staged")
     pool = rkc.Pool(cfgs, NBLK, C, Q, O, events_per_trace=EPT, device=local_rank)
     stream = torch.cuda.current_stream(dev)
     ev_cap = TRACES * EPT
@@ -349,10 +362,12 @@ def main():
         if dist_on:
             dist.all_reduce(hist_dev)
 
+    _phase("pool created")
     for _ in range(args.warmup):
         one_step()
     torch.cuda.synchronize()
 
+    _phase("warm-up done")
     # ---- timed region (device events; barrier + sync both sides) ----
     clk_path = os.path.join(tempfile.gettempdir(), f"rkc_clocks_{rank}.csv")
     sampler = clocks_sampler(clk_path, local_rank)
@@ -382,6 +397,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, step_kernel_ms = float(t[0]), float(t[1])
 
+    _phase("timed region done")
     # ---- e2e: the public C-ABI call with HOST buffers (pinned ops in, results out) ----
     # results land in pinned host memory (a user's choice the C ABI allows)
     counters_host = torch.zeros((TRACES, rkc.RKC_NCTR), dtype=torch.int32,
@@ -423,6 +439,7 @@ def main():
     h2d_gbs = 3 * probe.numel() / (h0.elapsed_time(h1) * 1e-3) / 1e9
     del probe_dev
 
+    _phase("e2e done")
     # ---- telemetry of one replay for the algorithmic byte model (outside timing) ----
     counters, events, hist = pool.read_all()
     ab = algorithmic_bytes(ops, counters, events)
@@ -468,6 +485,7 @@ def main():
     iss = issue_roofline(per_launch_ms * 1e3, (clk or {}).get("sm_mhz") or 0)
     if iss:
         out["roofline_issue"] = iss
+    _phase("telemetry + byte model done")
     if not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfgs, ops)
     print(json.dumps(out), flush=True)

@@ -522,7 +522,7 @@ rkc_status rkc_step_batch(rkc_pool* pool, const rkc_op* ops, uint32_t num_steps,
   size_t ramp = 2;
   while (done < num_steps) {
     const size_t lim = ramp < chunk ? ramp : chunk;
-    ramp *= 4;
+    if (ramp < chunk) ramp *= 4;  // (capped: no overflow over many chunks)
     const uint32_t n = (uint32_t)((num_steps - done) < lim ? (num_steps - done) : lim);
     CUDA_TRY(cudaStreamWaitEvent(pool->copy_stream, pool->ev_free[buf], 0));
     CUDA_TRY(cudaMemcpyAsync(pool->replay_buf[buf], ops + (size_t)done * T, (size_t)n * T * 16,
