@@ -504,7 +504,7 @@ rkc_status rkc_step_batch(rkc_pool* pool, const rkc_op* ops, uint32_t num_steps,
   // host op stream: double-buffered copies on the copy stream overlap the steps
   if (!pool->replay_buf[0]) {
     size_t per_step = (size_t)T * 16;
-    size_t steps = (64ull << 20) / per_step;
+    size_t steps = (256ull << 20) / per_step;  // 2 x 256 MB staging buffers
     if (steps < 1) steps = 1;
     pool->replay_steps = steps;
     for (int i = 0; i < 2; ++i) {
