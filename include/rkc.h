@@ -187,9 +187,15 @@ RKC_API int rkc_abi_version(void);
 RKC_API const char* rkc_status_string(rkc_status s);
 
 /* Create a pool: allocates and initialises every trace (all blocks FREE, no
- * claims / requests / objects, step 0).  per_trace: host array of
- * config->num_traces configs.  Errors: RKC_E_INVAL on out-of-range sizes or
- * policy bytes, RKC_E_NOMEM, RKC_E_CUDA.  On error *out is NULL. */
+ * claims / requests / objects, step 0).  The pool carries the runtime
+ * surface's "Usable KV capacity and headroom" (runtime-surface table: per
+ * trace U = usable_kv of the boundary) and the "Cache-equivalence
+ * identity" claims are compared against (G26).
+ * per_trace: host array of config->num_traces configs (U, policy bytes),
+ * read during the call only; the library owns every device buffer it
+ * allocates until rkc_pool_destroy.  Errors (no side effects): RKC_E_INVAL on
+ * out-of-range sizes or policy bytes, RKC_E_NOMEM, RKC_E_CUDA.  On error *out
+ * is NULL.  The caller's current CUDA device is left unchanged. */
 RKC_API rkc_status rkc_pool_create(const rkc_pool_config* config, const rkc_trace_config* per_trace,
                            rkc_pool** out);
 RKC_API rkc_status rkc_pool_destroy(rkc_pool* pool);
@@ -205,7 +211,13 @@ RKC_API rkc_status rkc_pool_info(const rkc_pool* pool, rkc_pool_config* config_o
  * rkc_op_stage).  Identity mismatch is folded into the op (G26). */
 RKC_API rkc_status rkc_claim_submit(rkc_pool* pool, const rkc_claim_input* claims, uint32_t n,
                             int on_device, void* stream);
-/* Stage ADMIT ops (active request admission; PEAK check G8). */
+/* Stage ADMIT ops: active request admission with the runtime surface's
+ * "Active live footprint estimate -- how much KV the active request must hold
+ * while being served" (runtime-surface table), checked at admission against
+ * the boundary P:504 under admit_check=PEAK (G8), and the "Future reusable
+ * admission decision" write_admit.  Host or device
+ * input array of n records; same staging rules and errors as
+ * rkc_claim_submit. */
 RKC_API rkc_status rkc_request_admit(rkc_pool* pool, const rkc_request_input* reqs, uint32_t n,
                              int on_device, void* stream);
 /* Stage arbitrary ops (ADVANCE / COMPLETE / INSERT / DEMOTE / TOUCH / ...).
@@ -216,7 +228,14 @@ RKC_API rkc_status rkc_request_admit(rkc_pool* pool, const rkc_request_input* re
 RKC_API rkc_status rkc_op_stage(rkc_pool* pool, const rkc_trace_op* ops, uint32_t n, int on_device,
                         void* stream);
 
-/* Run num_steps lockstep steps.
+/* Run num_steps lockstep steps.  One step per trace is the phase order
+ * expiry -> op -> post-op materialization pass around the
+ * feasibility boundary "protected_resident_kv + active_live_kv <= usable_kv"
+ * (sec. 3.4): when it holds the op is served with ordinary
+ * (claim-excluding) eviction; when it does not, "the runtime must choose an
+ * explicit action and should report that action at the claim level"
+ * -- auto-demotion, deferral or refusal with blocking-claim
+ * attribution.
  *   ops == NULL : num_steps must be 1; runs the staged slot, then clears it.
  *   ops != NULL : replay mode; ops is [num_steps][num_traces] rkc_op
  *                 (step-major).  on_device=0: host memory (copied through a

@@ -19,11 +19,12 @@ import pytest
 
 from oracle import oracle as orc
 from paper_2605_24259_b200.gen import (ADMIT, ADVANCE, COMPLETE, CONTRACT, DEMOTABLE, DEMOTE,
-                                       EXPIRING, HARD, HIT_ADMIT, INSERT, NATIVE, NONE, NOP, PEAK, SOFT,
+                                       EXPIRING, HARD, HIT_ADMIT, INSERT, NATIVE, NONE, NOP,
+                                       OFFLOADABLE, PEAK, SOFT,
                                        SOFT_LOWERING, SUBMIT, TOUCH, BEST_EFFORT, make_cfg, op,
                                        pack_ops)
 
-OBLIGATED = {HARD, DEMOTABLE, 3, EXPIRING}
+OBLIGATED = {HARD, DEMOTABLE, OFFLOADABLE, EXPIRING}
 
 
 def _candidates(view, cfg):
@@ -80,7 +81,7 @@ def _random_tiny_ops(rng, U, T):
         elif k == SUBMIT:
             F = rng.randint(1, U)
             ops.append(op(SUBMIT, rng.randrange(3), rng.randrange(4),
-                          rng.choice([SOFT, HARD, DEMOTABLE, EXPIRING, BEST_EFFORT]),
+                          rng.choice([SOFT, HARD, DEMOTABLE, OFFLOADABLE, EXPIRING, BEST_EFFORT]),
                           F, rng.randint(1, F), rng.randint(1, 6)))
         elif k == ADMIT:
             ops.append(op(ADMIT, rng.randrange(2), rng.randrange(4), rng.randrange(2),

@@ -114,7 +114,10 @@ def test_templates_closed_forms(suite_run):
             else:
                 R, A = p["R"], p["A"]
                 vR = max(0, A - (U - R))
-                assert c[orc.K["served"]] == 0 or True
+                # SOFT lowering protects nothing (P = 0, A <= U): the active
+                # request is never refused and gets all A blocks (C1)
+                assert c[orc.K["refused_protected"]] + c[orc.K["refused_capacity"]] == 0, p
+                assert c[orc.K["blocks_allocated"]] == R + A, p
                 assert c[orc.K["victims_claimed"]] == vR, p
                 assert c[orc.K["harmed_obligated"]] == (1 if vR > 0 else 0), p
         elif t == "L-MATFAIL":
