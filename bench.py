@@ -75,12 +75,12 @@ def select_workload(name: str):
 
 
 def shard(rank: int, world: int) -> tuple[int, int]:
-    """(first trace id, trace count) of this rank: weak scaling replays TRACES
-    per rank; strong scaling (c5) splits WL["traces"] over the ranks."""
-    if not WL.get("strong"):
-        return rank * TRACES, TRACES
-    total = WL["traces"]
-    lo, hi = total * rank // world, total * (rank + 1) // world
+    """(first trace id, trace count) of this rank (paper_2605_24259_b200/shard.py):
+    weak scaling replays WL["traces"] per rank; strong scaling (c5) splits
+    WL["traces"] over the ranks."""
+    from paper_2605_24259_b200.shard import shard_range, weak_range
+    lo, hi = (shard_range(rank, world, WL["traces"]) if WL.get("strong")
+              else weak_range(rank, WL["traces"]))
     return lo, hi - lo
 
 
@@ -92,12 +92,85 @@ def workload_config(n_gpus: int) -> dict:
     per = shard(0, n_gpus)[1]
     return {"workload": WL["desc"], "traces_per_gpu": per, "pool_blocks": NBLK,
             "steps_per_replay": TSTEPS,
-            "global_traces": WL["traces"] if WL.get("strong") else TRACES * n_gpus,
+            "global_traces": WL["traces"] if WL.get("strong") else WL["traces"] * n_gpus,
             "parallelism": f"trace-sharded x{n_gpus}", "l2": WL["l2"]}
 
 
 # --------------------------------------------------------------------------
-# algorithmic bytes of the step kernel (DESIGN.md sec. 4 "byte model")
+# algorithmic bytes of the lockstep step: SURVEY.md sec. 8(d) per-op table
+# --------------------------------------------------------------------------
+K_BLOCKS_ALLOCATED, K_ALLOCATIONS = 21, 30          # rkc.h RKC_CTR_*
+H_LANES = 128 + 128                                 # claim lanes + request lanes
+
+
+def survey_bytes(ops: np.ndarray, counters: np.ndarray, events: np.ndarray) -> dict:
+    """Bytes one full replay must move by SURVEY.md sec. 8(d)'s per-op table
+    (flat SoA layout: meta u32[N] + seq u32[N] + free bitmap N/8, header H =
+    claim lanes 128 B + request lanes 128 B).  Where the table gives an upper
+    bound ("<= 64") the bound is used for SUBMIT / DEMOTE and nothing for a
+    NOP; where a row depends on the outcome, the outcome comes from this
+    replay's own telemetry (events, counters):
+
+      every trace-step (NOP too)   reads 16 + H
+      SUBMIT / DEMOTE              writes 64
+      ADMIT / HIT_ADMIT            writes 32
+      ADVANCE without allocation   writes 32 (the request record; the table's
+                                   need <= free row with need = 0, no bitmap read)
+      allocation, need <= free     reads N/8, writes 4 need + 4 ceil(need/32) + 32
+                                   (ceil(need/32) >= 1 per allocation: 4 is used)
+      allocation with eviction     reads 4N + 4N + N/8, writes 4 k + 4 + 32
+                                   (+ 4 n seq words for an evicting INSERT)
+      COMPLETE                     reads 4N, writes 8 live (live >= blocks cached
+                                   or freed, from REQUEST_SERVED / WRITE_ADMISSION_DENIED)
+      TOUCH                        reads 4N, writes 4 L (L from REUSE_PROBE)
+      deferral / refusal           reads 4N (release of the request's blocks: not in
+                                   the table, counted like COMPLETE's scan)
+      HIT_ADMIT with h > 0 (f3)    reads 4N, writes 4 h (restamp, like TOUCH)
+      every event                  writes 32
+    """
+    T, n = ops.shape
+    N = NBLK
+    kind = ops["kind"]
+    et = events["type"]
+    cnt = {k: int((kind == k).sum()) for k in range(9)}
+    n_alloc = int(counters[:, K_ALLOCATIONS].astype(np.int64).sum())
+    k_all = int(counters[:, K_BLOCKS_ALLOCATED].astype(np.int64).sum())
+    vic = events[et == 12]
+    n_ev = len(vic)
+    k_ev = int(vic["f"][:, 3].astype(np.int64).sum())
+    k_ev_insert = int(vic[vic["reason"] == 1]["f"][:, 3].astype(np.int64).sum())
+    n_af, k_af = n_alloc - n_ev, k_all - k_ev
+    n_inserted = int(counters[:, 15].astype(np.int64).sum())
+    adv_alloc = n_alloc - n_inserted
+    served = events[et == 11]
+    denied = events[et == 10]
+    live_blocks = int(served[served["reason"] == 1]["f"][:, 1].astype(np.int64).sum()) + \
+        int(denied["f"][:, 1].astype(np.int64).sum())
+    probes = events[et == 13]
+    L_sum = int(probes["f"][:, 1].astype(np.int64).sum())
+    hits = events[et == 15]
+    hits_pos = hits[hits["f"][:, 1] > 0]
+    refusals = int(((et == 7) | (et == 8)).sum())
+    rd = n * T * (16 + H_LANES)
+    wr = 64 * (cnt[1] + cnt[6]) + 32 * (cnt[2] + cnt[8]) + 32 * max(0, cnt[3] - adv_alloc)
+    rd += n_af * (N // 8)
+    wr += 4 * k_af + n_af * (4 + 32)
+    rd += n_ev * (8 * N + N // 8)
+    wr += 4 * k_ev + n_ev * (4 + 32) + 4 * k_ev_insert
+    rd += len(served) * 4 * N
+    wr += 8 * live_blocks
+    rd += len(probes) * 4 * N
+    wr += 4 * L_sum
+    rd += refusals * 4 * N
+    rd += len(hits_pos) * 4 * N
+    wr += 4 * int(hits_pos["f"][:, 1].astype(np.int64).sum())
+    wr += 32 * len(events)
+    return dict(bytes=int(rd + wr), read=int(rd), write=int(wr), allocations=n_alloc,
+                evicting_selections=n_ev, events=len(events))
+
+
+# --------------------------------------------------------------------------
+# this layout's own byte model (DESIGN.md sec. 6), reported beside it
 # --------------------------------------------------------------------------
 def algorithmic_bytes(ops: np.ndarray, counters: np.ndarray, events: np.ndarray) -> dict:
     """Bytes the method must move in this layout for one full replay, by what
@@ -236,13 +309,89 @@ def issue_roofline(step_us: float, sm_mhz: float) -> dict | None:
 
 
 # --------------------------------------------------------------------------
-def cpu_baseline(cfgs, ops, budget_s: float = 12.0) -> dict:
+def host_info() -> dict:
+    """lscpu model / sockets x cores x threads and the oracle's compiler."""
+    info = {}
+    try:
+        out = subprocess.check_output(["lscpu"], text=True, env={**os.environ, "LC_ALL": "C"})
+        kv = {ln.split(":", 1)[0].strip(): ln.split(":", 1)[1].strip() for ln in out.splitlines()
+              if ":" in ln}
+        info = {"cpu_model": kv.get("Model name"), "sockets": kv.get("Socket(s)"),
+                "cores_per_socket": kv.get("Core(s) per socket"),
+                "threads_per_core": kv.get("Thread(s) per core"), "cpus": kv.get("CPU(s)"),
+                "numa_nodes": kv.get("NUMA node(s)")}
+    except Exception:
+        pass
+    try:
+        info["compiler"] = subprocess.check_output(["g++", "--version"], text=True).splitlines()[0]
+    except Exception:
+        info["compiler"] = None
+    info["flags"] = "-O2 -std=c++17 (no -march=native)"
+    return info
+
+
+def _compare_chunk(b, lo: int, hi: int, g_counters, g_events, g_idx) -> tuple[int, int]:
+    """(#traces whose events or counters differ, #events compared) for oracle batch b
+    holding traces [lo, hi) of this rank's pool."""
+    oe = b.events()
+    oe["trace"] += lo                                     # oracle trace ids are batch-local
+    ge = g_events[g_idx[lo]:g_idx[hi]]
+    bad = set()
+    if ge.tobytes() != oe.tobytes():
+        oi = np.searchsorted(oe["trace"], np.arange(lo, hi + 1))
+        for t in range(lo, hi):
+            a = ge[g_idx[t] - g_idx[lo]:g_idx[t + 1] - g_idx[lo]]
+            bb = oe[oi[t - lo]:oi[t - lo + 1]]
+            if a.tobytes() != bb.tobytes():
+                bad.add(t)
+    cd = np.nonzero((b.counters() != g_counters[lo:hi]).any(1))[0]
+    bad.update(int(lo + i) for i in cd)
+    return len(bad), len(oe)
+
+
+def _compare_views(pool, b, lo: int, n: int) -> bool:
+    """final state views (header, blocks, claims, requests, objects) of traces
+    [lo, lo + n): GPU export vs oracle export, byte for byte"""
+    g = pool.rkc_state_export(lo, n)
+    for i in range(n):
+        o = b.export(i)
+        for k in ("header", "blocks", "claims", "requests", "objects"):
+            if np.ascontiguousarray(g[k][i]).tobytes() != np.ascontiguousarray(o[k]).tobytes():
+                return False
+    return True
+
+
+def cpu_baseline(cfgs, ops, g_counters, g_events, pool, budget_s: float = 12.0,
+                 single_budget_s: float = 4.0) -> tuple[dict, dict]:
     """The oracle as it stands, on the host cores, on a bounded sample of the
-    same workload (the first traces of rank 0's shard)."""
+    same workload (the first traces of rank 0's shard): one figure on a single
+    core and one on every host core (SURVEY 8(d) "Oracle timing").  Outside
+    the timing, the oracle's results for the sampled traces are compared bit
+    for bit with the GPU's replay of the same traces in the bench's own pool
+    (events, counters, and the final state views of the first 64 traces)."""
     from oracle import oracle as orc
-    nthreads = os.cpu_count() or 1
-    chunk = max(64, 16 * nthreads) if WL["recipe"] == 3 else max(4, nthreads)
+    try:
+        os.sched_setaffinity(0, range(os.cpu_count() or 1))   # every host core for the oracle
+    except Exception:
+        pass
+    nthreads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    g_idx = np.searchsorted(g_events["trace"], np.arange(ops.shape[1] + 1))
+    checked, mism, ev_checked = 0, 0, 0
+    # single core
+    n1, ops1, t1 = 0, 0, 0.0
+    while t1 < single_budget_s and n1 < ops.shape[1]:
+        sl = slice(n1, min(n1 + 16, ops.shape[1]))
+        sub = np.ascontiguousarray(ops[:, sl])
+        b = orc.OracleBatch(cfgs[sl], NBLK, C, Q, O)
+        t0 = time.perf_counter()
+        b.run(sub, nthreads=1)
+        t1 += time.perf_counter() - t0
+        ops1 += int((sub["kind"] != 0).sum())
+        n1 = sl.stop
+    # all cores; every chunk is checked against the GPU after its timing
+    chunk = max(64, 16 * nthreads) if WL["recipe"] != 4 else max(4, nthreads)
     done_traces, ops_done, t_used = 0, 0, 0.0
+    views_ok = None
     while t_used < budget_s and done_traces < ops.shape[1]:
         sl = slice(done_traces, min(done_traces + chunk, ops.shape[1]))
         sub = np.ascontiguousarray(ops[:, sl])
@@ -251,12 +400,29 @@ def cpu_baseline(cfgs, ops, budget_s: float = 12.0) -> dict:
         b.run(sub, nthreads=nthreads)
         t_used += time.perf_counter() - t0
         ops_done += int((sub["kind"] != 0).sum())
+        m, ne = _compare_chunk(b, sl.start, sl.stop, g_counters, g_events, g_idx)
+        mism += m
+        ev_checked += ne
+        checked += sl.stop - sl.start
+        if views_ok is None:
+            nv = min(64, sl.stop - sl.start)
+            views_ok = _compare_views(pool, b, sl.start, nv)
         done_traces = sl.stop
-    return {"value": ops_done / t_used, "unit": UNIT, "cores": nthreads, "kind": "oracle",
+    base = {"value": ops_done / t_used, "unit": UNIT, "cores": nthreads, "kind": "oracle",
             "sample": f"first {done_traces} traces of the {WL['desc'][:2]} workload x {TSTEPS} steps "
-                      f"({ops_done} non-NOP ops) in {t_used:.1f} s, plain C++ oracle (-O2), "
+                      f"({ops_done} non-NOP ops) in {t_used:.1f} s, plain C++ oracle, "
                       f"{nthreads} threads, one trace per task",
-            "traces_per_s": done_traces / t_used}
+            "traces_per_s": done_traces / t_used,
+            "single_core": {"value": ops1 / t1, "unit": UNIT, "cores": 1,
+                            "sample": f"first {n1} traces x {TSTEPS} steps ({ops1} non-NOP ops) "
+                                      f"in {t1:.1f} s"},
+            "host": host_info()}
+    parity = {"status": "sampled-bit-exact" if mism == 0 and views_ok else "MISMATCH",
+              "traces_checked": checked, "events_checked": ev_checked,
+              "traces_mismatched": mism, "state_views_first_64": bool(views_ok),
+              "what": "the oracle's events (trace, step, seq order), counters and final state "
+                      "views vs the GPU replay of the same traces in the bench's own pool"}
+    return base, parity
 
 
 def run_reference(args, rank: int, world: int):
@@ -294,6 +460,46 @@ def run_reference(args, rank: int, world: int):
 
 
 # --------------------------------------------------------------------------
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def respawn_ranks(n: int) -> int:
+    """`python bench.py --gpus N` without a launcher: re-run this command under
+    torchrun with N ranks on this node (rendezvous on 127.0.0.1), the same
+    launch the driver uses; returns torchrun's exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def bind_numa(gpu: int) -> dict:
+    """Bind this process to the CPUs of the GPU's NUMA node (pinned host
+    buffers are then allocated node-locally); returns what was found."""
+    out = {"numa_node": None, "bound_cpus": None}
+    try:
+        bus = subprocess.check_output(["nvidia-smi", "-i", str(gpu), "--query-gpu=pci.bus_id",
+                                       "--format=csv,noheader"], text=True).strip()
+        dom, rest = bus.split(":", 1)
+        path = f"/sys/bus/pci/devices/{dom[-4:].lower()}:{rest.lower()}/numa_node"
+        node = int(open(path).read().strip())
+        out["numa_node"] = node
+        if node >= 0:
+            cpus = set()
+            for part in open(f"/sys/devices/system/node/node{node}/cpulist").read().strip().split(","):
+                a, _, b = part.partition("-")
+                cpus.update(range(int(a), int(b or a) + 1))
+            os.sched_setaffinity(0, cpus)
+            out["bound_cpus"] = len(cpus)
+    except Exception:
+        pass
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -307,8 +513,10 @@ def main():
     select_workload(args.config)
     args.warmup = max(3, args.warmup)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(respawn_ranks(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank, world)
@@ -316,23 +524,29 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2605_24259_b200 import build, gen
-    build.build()
-    from paper_2605_24259_b200 import rkc
+    if rank == 0:                 # the other ranks wait at the barrier below
+        build.build()
+        gen.build()
+    from paper_2605_24259_b200.shard import allreduce_histogram
 
-    # one process per GPU; RKC_BENCH_SAME_GPU=1 + RKC_DIST_BACKEND=gloo lets the
-    # multi-rank path be exercised with several ranks on one device (testing only)
+    # one process per GPU over NCCL.  With fewer GPUs than ranks (e.g. the
+    # 1-GPU lease), ranks share devices round-robin over gloo: the multi-rank
+    # path runs end to end, but the numbers are time-sliced, not a scaling point.
     ndev = torch.cuda.device_count()
-    gpu = local_rank if not os.environ.get("RKC_BENCH_SAME_GPU") else local_rank % max(1, ndev)
+    oversub = world > ndev or bool(os.environ.get("RKC_BENCH_SAME_GPU"))
+    gpu = local_rank % max(1, ndev)
     torch.cuda.set_device(gpu)
     dist_on = world > 1
     if dist_on:
-        backend = os.environ.get("RKC_DIST_BACKEND", "nccl")
+        backend = os.environ.get("RKC_DIST_BACKEND", "gloo" if oversub else "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
         else:
             dist.init_process_group(backend)
+        dist.barrier()
+    from paper_2605_24259_b200 import rkc
+    host = bind_numa(gpu)
     dev = torch.device("cuda", gpu)
-    local_rank = gpu
 
     # ---- inputs: this rank's shard, generated on the host, resident in HBM ----
     global TRACES
@@ -345,7 +559,7 @@ def main():
     ops_pinned = torch.empty(ops_u8.size, dtype=torch.uint8, pin_memory=True)
     ops_pinned.numpy()[:] = ops_u8
     _phase("inputs generated and staged")
-    pool = rkc.Pool(cfgs, NBLK, C, Q, O, events_per_trace=EPT, device=local_rank)
+    pool = rkc.Pool(cfgs, NBLK, C, Q, O, events_per_trace=EPT, device=gpu)
     stream = torch.cuda.current_stream(dev)
     ev_cap = TRACES * EPT
     events_dev = torch.empty(ev_cap * 32, dtype=torch.uint8, device=dev)
@@ -360,7 +574,7 @@ def main():
             ev_pair[1].record(stream)
         pool.rkc_telemetry_read(events_out=events_dev, hist_out=hist_dev, stream=stream)
         if dist_on:
-            dist.all_reduce(hist_dev)
+            allreduce_histogram(hist_dev)
 
     _phase("pool created")
     for _ in range(args.warmup):
@@ -370,7 +584,7 @@ def main():
     _phase("warm-up done")
     # ---- timed region (device events; barrier + sync both sides) ----
     clk_path = os.path.join(tempfile.gettempdir(), f"rkc_clocks_{rank}.csv")
-    sampler = clocks_sampler(clk_path, local_rank)
+    sampler = clocks_sampler(clk_path, gpu)
     time.sleep(0.3)
     pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
              for _ in range(args.steps)]
@@ -407,24 +621,46 @@ def main():
     # first use and the pinned pages are touched once
     pool.rkc_pool_reset(stream)
     _step_host(pool, ops_pinned, stream)
-    pool.rkc_telemetry_read(counters_out=counters_host, hist_out=hist_host, stream=stream)
-    if dist_on:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.e2e_steps):
+    _, n_events = pool.rkc_telemetry_read(counters_out=counters_host, hist_out=hist_host,
+                                          stream=stream)
+
+    def e2e_pass(events_host=None) -> float:
+        if dist_on:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         pool.rkc_pool_reset(stream)
         _step_host(pool, ops_pinned, stream)
-        pool.rkc_telemetry_read(counters_out=counters_host, hist_out=hist_host, stream=stream)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
-    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    if dist_on:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_ms = float(te[0])
+        pool.rkc_telemetry_read(counters_out=counters_host, events_out=events_host,
+                                hist_out=hist_host, stream=stream)
+        if dist_on:                                        # the histogram SUM over ranks
+            hd = torch.from_numpy(hist_host).to(dev)
+            allreduce_histogram(hd)
+            hist_host[:] = hd.cpu().numpy()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if dist_on:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        return float(te[0])
+
+    e2e_all = [e2e_pass() for _ in range(max(3, args.e2e_steps))]
+    e2e_ms = float(np.median(e2e_all))
+    # the same with the compacted claim-level event stream read back too (the
+    # paper's telemetry), when host memory allows a pinned buffer
+    ev_bytes = int(n_events) * 32
+    e2e_ev_ms = None
+    try:
+        avail = int([ln.split()[1] for ln in open("/proc/meminfo")
+                     if ln.startswith("MemAvailable")][0]) * 1024
+    except Exception:
+        avail = 0
+    if ev_bytes and ev_bytes < avail // 4:
+        events_host = torch.empty(ev_bytes, dtype=torch.uint8, pin_memory=True).numpy()
+        e2e_pass(events_host)                              # touch the pages once
+        e2e_ev_ms = float(np.median([e2e_pass(events_host) for _ in range(3)]))
+        del events_host
     # this box's pinned host->device copy bandwidth (the e2e floor is
     # h2d_bytes_per_step / h2d_gbs when the copies outrun the steps)
     probe = ops_pinned[: min(ops_pinned.numel(), 256 << 20)]
@@ -440,22 +676,33 @@ def main():
     del probe_dev
 
     _phase("e2e done")
-    # ---- telemetry of one replay for the algorithmic byte model (outside timing) ----
+    # ---- telemetry of one replay for the algorithmic byte models (outside timing) ----
     counters, events, hist = pool.read_all()
+    sb = survey_bytes(ops, counters, events)
     ab = algorithmic_bytes(ops, counters, events)
-    tot = torch.tensor([non_nop, TRACES], dtype=torch.float64, device=dev)
+    tot = torch.tensor([non_nop, TRACES, len(events), sb["bytes"], ab["bytes"]],
+                       dtype=torch.float64, device=dev)
     if dist_on:
         dist.all_reduce(tot)
-    total_events, total_traces = float(tot[0]), float(tot[1])
+    total_events, total_traces, total_records = float(tot[0]), float(tot[1]), float(tot[2])
+    survey_total, layout_total = float(tot[3]), float(tot[4])
 
     clk = clocks_summary(clk_path)
+    parity = None
+    if rank == 0 and not args.no_cpu_baseline:
+        _phase("cpu baseline + sampled parity")
+        cpu, parity = cpu_baseline(cfgs, ops, counters, events, pool)
+    if dist_on:
+        dist.barrier()
     if rank != 0:
         if dist_on:
             dist.destroy_process_group()
         return
     peak, peak_src = load_peak()
     per_launch_ms = step_kernel_ms / (args.steps * TSTEPS)
-    achieved = ab["bytes"] / TSTEPS / (per_launch_ms * 1e-3) / 1e9
+    # every rank's lockstep step runs concurrently: bytes of all ranks / the max step time
+    achieved = survey_total / TSTEPS / (per_launch_ms * 1e-3) / 1e9
+    achieved_layout = layout_total / TSTEPS / (per_launch_ms * 1e-3) / 1e9
     traffic = load_traffic()
     value = total_events * args.steps / (ms * 1e-3)
     out = {
@@ -464,30 +711,47 @@ def main():
         "scaling": scaling(), "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": workload_config(world),
         "traces_per_s": total_traces * args.steps / (ms * 1e-3),
+        "telemetry_records_per_s": total_records * args.steps / (ms * 1e-3),
         "events_per_step": total_events,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "lockstep step: rkc_light_kernel + rkc_step_kernel + rkc_step_overflow_kernel",
                      "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": ab["bytes"] / TSTEPS,
+                     "byte_model": "SURVEY.md 8(d) per-op table (bench.py survey_bytes)",
+                     "algorithmic_bytes_per_launch": survey_total / TSTEPS,
                      "avg_launch_us": per_launch_ms * 1e3,
-                     "step_kernel_share": step_kernel_ms / ms},
+                     "step_kernel_share": step_kernel_ms / ms,
+                     "layout_model": {"bytes_per_launch": layout_total / TSTEPS,
+                                      "achieved": achieved_layout, "frac": achieved_layout / peak,
+                                      "what": "this layout's own byte model (DESIGN.md sec. 6)"}},
         "e2e": {"value": total_events / (e2e_ms * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": int(ops_u8.size),
                 "d2h_bytes_per_step": int(counters_host.nbytes + hist_host.nbytes),
-                "ms_per_step": e2e_ms,
+                "ms_per_step": e2e_ms, "passes_ms": e2e_all, "stat": "median",
                 "h2d_gbs_measured": h2d_gbs,
                 "path": "rkc_pool_reset + rkc_step_batch(pinned host ops) + "
                         "rkc_telemetry_read(host counters + histogram)"},
         "gpu_launches": int(launches),
         "clocks": clk,
+        "host": host,
     }
+    if e2e_ev_ms is not None:
+        out["e2e_with_events"] = {
+            "value": total_events / (e2e_ev_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ev_ms,
+            "h2d_bytes_per_step": int(ops_u8.size),
+            "d2h_bytes_per_step": int(counters_host.nbytes + hist_host.nbytes + ev_bytes),
+            "path": "as e2e, plus the compacted claim-level event stream read into pinned host memory"}
+    if oversub:
+        out["oversubscribed"] = (f"{world} ranks share {ndev} GPU(s) over gloo: the multi-rank "
+                                 "path end to end, time-sliced, not a scaling figure")
     iss = issue_roofline(per_launch_ms * 1e3, (clk or {}).get("sm_mhz") or 0)
     if iss:
         out["roofline_issue"] = iss
     _phase("telemetry + byte model done")
-    if not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(cfgs, ops)
+    if parity is not None:
+        out["cpu_baseline"] = cpu
+        out["parity"] = parity["status"]
+        out["parity_detail"] = parity
     print(json.dumps(out), flush=True)
     if dist_on:
         dist.destroy_process_group()

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define RKC_ABI_VERSION 1
+#define RKC_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define RKC_API __attribute__((visibility("default")))
@@ -102,7 +102,8 @@ enum { RKC_CTR_OPS = 0, RKC_CTR_ACCEPTED, RKC_CTR_REJECTED, RKC_CTR_MATERIALIZED
        RKC_CTR_VICTIMS_ORDINARY, RKC_CTR_VICTIMS_AFTER_RELEASE, RKC_CTR_VICTIMS_CLAIMED,
        RKC_CTR_BLOCKS_ALLOCATED, RKC_CTR_BLOCKS_CACHED, RKC_CTR_REUSE_PROBES,
        RKC_CTR_REUSE_TOKENS, RKC_CTR_OP_ERRORS, RKC_CTR_STEPS, RKC_CTR_EVENTS,
-       RKC_CTR_PREFIX_HITS, RKC_CTR_HIT_TOKENS /* f3 */ };
+       RKC_CTR_PREFIX_HITS, RKC_CTR_HIT_TOKENS /* f3 */,
+       RKC_CTR_ALLOCATIONS /* successful allocations (free-only or evicting) */ };
 /* outcome histogram (int64[RKC_NHIST]):
  *   [0, 42)   final claim state (7) x mode (6): index state*6 + mode
  *   [42, 47)  final request status (5)
@@ -206,9 +207,10 @@ RKC_API rkc_status rkc_pool_info(const rkc_pool* pool, rkc_pool_config* config_o
                          uint64_t* device_bytes_out);
 
 /* Stage SUBMIT ops (claim decision) for the next single step.  A
- * trace may receive at most one staged op per step; a second one for the same
- * trace is RKC_E_INVAL (host input: nothing staged; device input: see
- * rkc_op_stage).  Identity mismatch is folded into the op (G26). */
+ * trace may receive at most one staged op per step; with host input, a
+ * second one for the same trace -- in this call or in any host staging call
+ * since the last step -- is RKC_E_INVAL with nothing staged (device input:
+ * see rkc_op_stage).  Identity mismatch is folded into the op (G26). */
 RKC_API rkc_status rkc_claim_submit(rkc_pool* pool, const rkc_claim_input* claims, uint32_t n,
                             int on_device, void* stream);
 /* Stage ADMIT ops: active request admission with the runtime surface's
@@ -252,10 +254,18 @@ RKC_API rkc_status rkc_step_batch(rkc_pool* pool, const rkc_op* ops, uint32_t nu
  *   hist_out:     int64[RKC_NHIST] outcome histogram or NULL
  *   on_device:    outputs are device pointers (else host; the call then
  *                 synchronises the stream)
- *   drain:        clear the event buffers after a successful read
+ *   drain:        empty the per-trace event rings after a successful read;
+ *                 later reads return only events emitted after the drain
+ *                 (RKC_CTR_EVENTS stays the emitted total since creation /
+ *                 reset, and rkc_pool_conformance then checks the drained
+ *                 traces from "unknown" claim states, without the
+ *                 final-state comparison)
  * RKC_E_OVERFLOW: events_cap < total -- nothing copied, *events_written =
  * total.  RKC_E_LOST: some trace overflowed events_per_trace (outputs are
- * still written; the counter RKC_CTR_EVENTS holds the emitted total). */
+ * still written; the counter RKC_CTR_EVENTS holds the emitted total).
+ * Outputs are caller-owned; the call runs on the pool's device (the caller's
+ * current device is left unchanged) and is bracketed by an NVTX range, as is
+ * rkc_step_batch. */
 RKC_API rkc_status rkc_telemetry_read(rkc_pool* pool, uint32_t* counters_out, rkc_event* events_out,
                               uint64_t events_cap, uint64_t* events_written, int64_t* hist_out,
                               int on_device, int drain, void* stream);
@@ -268,8 +278,12 @@ RKC_API rkc_status rkc_state_export(rkc_pool* pool, uint32_t trace_begin, uint32
                             rkc_claim_view* claims, rkc_request_view* requests,
                             rkc_object_view* objects);
 /* Test-only state injection (e.g. the L6 fixture): derived
- * device state (keys, leading prefixes, protected counts, free bitmap) is
- * recomputed from the views.  seq_ctr per trace from headers[i].seq_ctr. */
+ * device state (keys, protected counts, free bitmap, header counts) is
+ * recomputed from the views, and the leading prefix of every live object
+ * (the materialization predicate) by a kernel on the device.
+ * seq_ctr per trace from headers[i].seq_ctr.  Every view is validated first
+ * (states / modes / statuses in range, owner < O or Q, claim < C or 0xFF,
+ * cached pos < len of a live object): RKC_E_INVAL with nothing written. */
 RKC_API rkc_status rkc_state_import(rkc_pool* pool, uint32_t trace_begin, uint32_t n,
                             const rkc_header_view* headers, const rkc_block_view* blocks,
                             const rkc_claim_view* claims, const rkc_request_view* requests,
@@ -278,7 +292,7 @@ RKC_API rkc_status rkc_state_import(rkc_pool* pool, uint32_t trace_begin, uint32
 /* ---- conformance ---------------------------
  * Per-trace replay of the claim-level event stream reconstructing every
  * claim's lifecycle.  verdict bit set = check FAILED for that trace. */
-#define RKC_CHECK_L1 0x01u   /* harm only after acceptance + materialization      */
+#define RKC_CHECK_L1 0x01u   /* harm only after acceptance                */
 #define RKC_CHECK_L2 0x02u   /* write-admission denial followed by service        */
 #define RKC_CHECK_L3 0x04u   /* refusal capacity proof and blocking attribution   */
 #define RKC_CHECK_L45 0x08u  /* release (demote / expire) before loss, no harm    */
@@ -292,9 +306,11 @@ RKC_API rkc_status rkc_state_import(rkc_pool* pool, uint32_t trace_begin, uint32
 #define RKC_NEVIDENCE 9
 /* Check a compacted event stream (device pointers): events in (trace, step,
  * seq) order, offsets [num_traces+1] exclusive prefix, optional final claim
- * states [num_traces][claims_per_trace] (u8) and lowering bytes [num_traces].
- * verdict_out [num_traces] u32 and evidence_out int64[RKC_NEVIDENCE] are
- * device pointers (evidence is accumulated: zero it first). */
+ * states [num_traces][claims_per_trace] (u8) and lowering bytes [num_traces]
+ * (I4 is checked only when lowering is given).  verdict_out [num_traces] u32
+ * and evidence_out int64[RKC_NEVIDENCE] are device pointers (evidence is
+ * accumulated: zero it first).  Legal lifecycle per S:44 / S:66-68 (accepted
+ * -> harmed included). */
 RKC_API rkc_status rkc_conformance_check(const rkc_event* events, const uint32_t* offsets,
                                          uint32_t num_traces, const uint8_t* final_claim_states,
                                          uint32_t claims_per_trace, const uint8_t* lowering,

@@ -38,7 +38,7 @@ COUNTER_NAMES = [
     "deferred_capacity", "refused_protected", "refused_capacity", "inserted", "insert_refused",
     "write_denied", "victims_ordinary", "victims_after_release", "victims_claimed",
     "blocks_allocated", "blocks_cached", "reuse_probes", "reuse_tokens", "op_errors", "steps",
-    "events", "prefix_hits", "hit_tokens"]
+    "events", "prefix_hits", "hit_tokens", "allocations"]
 K = {n: i for i, n in enumerate(COUNTER_NAMES)}
 
 # event types

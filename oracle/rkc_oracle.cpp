@@ -72,7 +72,8 @@ enum { K_OPS = 0, K_ACCEPTED, K_REJECTED, K_MATERIALIZED, K_DEMOTED_EXPLICIT, K_
        K_DEFERRED_PROTECTED, K_DEFERRED_CAPACITY, K_REFUSED_PROTECTED, K_REFUSED_CAPACITY,
        K_INSERTED, K_INSERT_REFUSED, K_WRITE_DENIED, K_VICTIMS_ORDINARY, K_VICTIMS_AFTER_RELEASE,
        K_VICTIMS_CLAIMED, K_BLOCKS_ALLOCATED, K_BLOCKS_CACHED, K_REUSE_PROBES, K_REUSE_TOKENS,
-       K_OP_ERRORS, K_STEPS, K_EVENTS, K_PREFIX_HITS, K_HIT_TOKENS, K_NCOUNTERS = 32 };
+       K_OP_ERRORS, K_STEPS, K_EVENTS, K_PREFIX_HITS, K_HIT_TOKENS, K_ALLOCATIONS,
+       K_NCOUNTERS = 32 };
 
 const uint32_t BLOCK_TOKENS = 16;              /* P:615 "16-token block size" */
 const uint32_t NO_OBJ_CLAIM = 0xFF;            /* object has no claim binding */
@@ -220,12 +221,13 @@ struct Trace {
    * reusable; never exceeds len. */
   uint32_t leading(uint32_t o) const {
     if (!obj[o].live) return 0;
-    for (uint32_t p = 0; p < obj[o].len; ++p) {
-      bool present = false;
-      for (uint32_t b = 0; b < blk.size(); ++b)
-        if (blk[b].res == B_CACHED && blk[b].owner == o && blk[b].pos == p) { present = true; break; }
-      if (!present) return p;
-    }
+    /* one pass over the blocks marks the cached positions of o, then the
+     * first unmarked position is the answer (same definition, O(N + len)) */
+    std::vector<char> present(obj[o].len, 0);
+    for (uint32_t b = 0; b < blk.size(); ++b)
+      if (blk[b].res == B_CACHED && blk[b].owner == o && blk[b].pos < obj[o].len) present[blk[b].pos] = 1;
+    for (uint32_t p = 0; p < obj[o].len; ++p)
+      if (!present[p]) return p;
     return obj[o].len;
   }
   /* P = protected_resident_kv. */
@@ -371,6 +373,7 @@ struct Trace {
     ctr[K_VICTIMS_AFTER_RELEASE] += after_release;
     ctr[K_VICTIMS_CLAIMED] += claimed_v;
     ctr[K_BLOCKS_ALLOCATED] += k;
+    ctr[K_ALLOCATIONS]++;  /* successful alloc calls (measurement: SURVEY 8(d) rows) */
     if (ordinary + after_release + claimed_v > 0)
       emit(E_VICTIMS, slot, reason_kind, 0, ordinary, after_release, claimed_v, k);
     return taken;

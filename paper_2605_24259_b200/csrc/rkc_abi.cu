@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <cub/device/device_scan.cuh>
+#include <nvtx3/nvToolsExt.h>
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -62,7 +64,27 @@ struct rkc_pool {
   uint64_t step = 0;
   uint32_t stage_calls = 0;      // staging calls since the last step
   bool staged_any = false;
+  std::vector<uint8_t> host_staged;  // traces staged from host input since the last step
   size_t device_bytes = 0;
+};
+
+// Every entry point runs on the pool's device and leaves the caller's current
+// device as it found it.
+struct DeviceGuard {
+  int prev = -1;
+  bool changed = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) changed = cudaSetDevice(dev) == cudaSuccess;
+    cudaGetLastError();
+  }
+  ~DeviceGuard() { if (changed) cudaSetDevice(prev); }
+};
+#define RKC_ON_DEVICE(pool) DeviceGuard rkc_guard_((pool)->cfg.device)
+
+// NVTX range for profilers (header-only NVTX3: no cost without a tool attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
 };
 
 #define CUDA_TRY(x)                          \
@@ -199,10 +221,16 @@ __global__ void event_gather_kernel(PoolDev p, const uint32_t* counts, const uin
     for (uint32_t i = lane; i < n; i += 32) dst[i] = src[i];
   }
 }
+// drain: the ring restarts empty; the drained count moves to H_EVDRAINED so
+// the emitted total (RKC_CTR_EVENTS) stays monotonic and the conformance pass
+// knows the ring no longer holds the whole history
 __global__ void drain_kernel(PoolDev p) {
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < p.num_traces;
-       t += gridDim.x * blockDim.x)
-    p.hdr[(size_t)t * H_NWORDS + H_EVCOUNT] = 0;
+       t += gridDim.x * blockDim.x) {
+    uint32_t* h = p.hdr + (size_t)t * H_NWORDS;
+    h[H_EVDRAINED] += h[H_EVCOUNT];
+    h[H_EVCOUNT] = 0;
+  }
 }
 __global__ void counters_kernel(PoolDev p, uint64_t step, uint32_t* out) {
   const size_t total = (size_t)p.num_traces * K_NCTR;
@@ -211,7 +239,7 @@ __global__ void counters_kernel(PoolDev p, uint64_t step, uint32_t* out) {
     const uint32_t t = (uint32_t)(i / K_NCTR), k = (uint32_t)(i % K_NCTR);
     uint32_t v = p.ctr[i];
     if (k == K_STEPS) v = (uint32_t)step;
-    if (k == K_EVENTS) v = p.hdr[(size_t)t * H_NWORDS + H_EVCOUNT];
+    if (k == K_EVENTS) v = p.hdr[(size_t)t * H_NWORDS + H_EVCOUNT] + p.hdr[(size_t)t * H_NWORDS + H_EVDRAINED];
     out[i] = v;
   }
 }
@@ -234,7 +262,7 @@ __global__ void hist_kernel(PoolDev p, uint64_t step, unsigned long long* hist) 
     for (uint32_t k = 0; k < K_NCTR; ++k) {
       uint64_t v = p.ctr[(size_t)t * K_NCTR + k];
       if (k == K_STEPS) v = step;
-      if (k == K_EVENTS) v = p.hdr[(size_t)t * H_NWORDS + H_EVCOUNT];
+      if (k == K_EVENTS) v = (uint64_t)p.hdr[(size_t)t * H_NWORDS + H_EVCOUNT] + p.hdr[(size_t)t * H_NWORDS + H_EVDRAINED];
       if (v) atomicAdd(&sh[RKC_HIST_CTR + k], (unsigned long long)v);
     }
   }
@@ -275,6 +303,7 @@ rkc_status run_init(rkc_pool* p, cudaStream_t st) {
   p->step = 0;
   p->stage_calls = 0;
   p->staged_any = false;
+  std::fill(p->host_staged.begin(), p->host_staged.end(), 0);
   return RKC_OK;
 }
 
@@ -294,18 +323,23 @@ rkc_status stage_common(rkc_pool* p, Kernel k, const In* in, uint32_t n, int on_
                         cudaStream_t st, bool with_identity) {
   if (!p || (!in && n > 0)) return RKC_E_INVAL;
   if (n == 0) return RKC_OK;
+  RKC_ON_DEVICE(p);
   if (n >= (1u << 24) || p->stage_calls >= 255) return RKC_E_INVAL;
   const uint32_t T = p->d.num_traces;
   const In* src = in;
   void* tmp_in = nullptr;
   if (!on_device) {
-    // host input: reject duplicates / out-of-range traces with no side effect
+    // host input: reject duplicates / out-of-range traces, within this call
+    // and against every host staging call since the last step, with no side
+    // effect (device input is resolved on the device, see rkc_op_stage)
+    if (p->host_staged.size() != T) p->host_staged.assign(T, 0);
     std::vector<uint8_t> seen(T, 0);
     for (uint32_t i = 0; i < n; ++i) {
       const uint32_t t = in[i].trace;
-      if (t >= T || seen[t]) return RKC_E_INVAL;
+      if (t >= T || seen[t] || p->host_staged[t]) return RKC_E_INVAL;
       seen[t] = 1;
     }
+    for (uint32_t i = 0; i < n; ++i) p->host_staged[in[i].trace] = 1;
     CUDA_TRY(cudaMallocAsync(&tmp_in, sizeof(In) * n, st));
     CUDA_TRY(cudaMemcpyAsync(tmp_in, in, sizeof(In) * n, cudaMemcpyHostToDevice, st));
     src = (const In*)tmp_in;
@@ -367,7 +401,12 @@ rkc_status rkc_pool_create(const rkc_pool_config* config, const rkc_trace_config
         tc.admit_check > 1 || tc.auto_demote > 1 || tc.accept_rule > 1)
       return RKC_E_INVAL;
   }
-  if (cudaSetDevice(c.device) != cudaSuccess) { cudaGetLastError(); return RKC_E_CUDA; }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || c.device < 0 || c.device >= ndev) {
+    cudaGetLastError();
+    return c.device < 0 || (ndev > 0 && c.device >= ndev) ? RKC_E_INVAL : RKC_E_CUDA;
+  }
+  DeviceGuard guard(c.device);
   rkc_pool* p = new (std::nothrow) rkc_pool();
   if (!p) return RKC_E_NOMEM;
   p->cfg = c;
@@ -437,6 +476,7 @@ rkc_status rkc_pool_create(const rkc_pool_config* config, const rkc_trace_config
 
 rkc_status rkc_pool_destroy(rkc_pool* pool) {
   if (!pool) return RKC_E_INVAL;
+  RKC_ON_DEVICE(pool);
   cudaDeviceSynchronize();
   free_all(pool);
   delete pool;
@@ -445,6 +485,7 @@ rkc_status rkc_pool_destroy(rkc_pool* pool) {
 
 rkc_status rkc_pool_reset(rkc_pool* pool, void* stream) {
   if (!pool) return RKC_E_INVAL;
+  RKC_ON_DEVICE(pool);
   return run_init(pool, (cudaStream_t)stream);
 }
 
@@ -459,6 +500,7 @@ rkc_status rkc_pool_info(const rkc_pool* pool, rkc_pool_config* config_out, uint
 
 rkc_status rkc_staging_conflicts(rkc_pool* pool, uint64_t* out) {
   if (!pool || !out) return RKC_E_INVAL;
+  RKC_ON_DEVICE(pool);
   unsigned long long v = 0;
   CUDA_TRY(cudaMemcpy(&v, pool->conflicts, 8, cudaMemcpyDeviceToHost));
   *out = v;
@@ -481,6 +523,8 @@ rkc_status rkc_op_stage(rkc_pool* pool, const rkc_trace_op* ops, uint32_t n, int
 rkc_status rkc_step_batch(rkc_pool* pool, const rkc_op* ops, uint32_t num_steps, int on_device,
                           void* stream) {
   if (!pool) return RKC_E_INVAL;
+  RKC_ON_DEVICE(pool);
+  NvtxRange nvtx("rkc_step_batch");
   cudaStream_t st = (cudaStream_t)stream;
   const uint32_t T = pool->d.num_traces;
   if (!ops) {
@@ -491,6 +535,7 @@ rkc_status rkc_step_batch(rkc_pool* pool, const rkc_op* ops, uint32_t num_steps,
     pool->step += 1;
     pool->stage_calls = 0;
     pool->staged_any = false;
+    std::fill(pool->host_staged.begin(), pool->host_staged.end(), 0);
     return RKC_OK;
   }
   if (pool->staged_any) return RKC_E_STATE;  // staged ops pending: run them first
@@ -544,6 +589,8 @@ rkc_status rkc_telemetry_read(rkc_pool* pool, uint32_t* counters_out, rkc_event*
                               uint64_t events_cap, uint64_t* events_written, int64_t* hist_out,
                               int on_device, int drain, void* stream) {
   if (!pool) return RKC_E_INVAL;
+  RKC_ON_DEVICE(pool);
+  NvtxRange nvtx("rkc_telemetry_read");
   cudaStream_t st = (cudaStream_t)stream;
   const PoolDev& d = pool->d;
   const size_t T = d.num_traces;
@@ -616,6 +663,7 @@ rkc_status rkc_state_export(rkc_pool* pool, uint32_t trace_begin, uint32_t n,
                             rkc_claim_view* claims, rkc_request_view* requests,
                             rkc_object_view* objects) {
   if (!pool || trace_begin + (uint64_t)n > pool->d.num_traces) return RKC_E_INVAL;
+  RKC_ON_DEVICE(pool);
   const PoolDev& d = pool->d;
   const uint32_t N = pool->cfg.max_blocks, NS = d.NS;
   std::vector<uint32_t> key((size_t)n * NS), meta((size_t)n * NS), hdr((size_t)n * H_NWORDS),
@@ -684,6 +732,79 @@ rkc_status rkc_state_export(rkc_pool* pool, uint32_t trace_begin, uint32_t n,
   return RKC_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// state import, step 1: every view is checked before anything is indexed or
+// written (a malformed view is RKC_E_INVAL with no side effect)
+static bool views_valid(const rkc_pool* pool, uint32_t U, const rkc_block_view* bv,
+                        const rkc_claim_view* cv, const rkc_request_view* rv,
+                        const rkc_object_view* ov) {
+  const PoolDev& d = pool->d;
+  for (uint32_t o = 0; o < d.O; ++o) {
+    if (ov[o].live > 1 || ov[o].len >= (1u << 22)) return false;
+    if (ov[o].claim != 0xFF && ov[o].claim >= d.C) return false;
+  }
+  for (uint32_t c = 0; c < d.C; ++c)
+    if (cv[c].state > C_HARMED || cv[c].mode > M_BEST_EFFORT || cv[c].obj >= d.O) return false;
+  for (uint32_t r = 0; r < d.Q; ++r)
+    if (rv[r].status > R_COMPLETED || rv[r].target >= d.O || rv[r].write_admit > 1) return false;
+  for (uint32_t b = 0; b < U; ++b) {
+    const rkc_block_view& v = bv[b];
+    if (v.res == kResCached) {
+      if (v.owner >= d.O || v.pos >= ov[v.owner].len || !ov[v.owner].live) return false;
+    } else if (v.res == kResActive) {
+      if (v.owner >= d.Q || v.pos >= (1u << 22)) return false;
+    } else if (v.res != kResFree) {
+      return false;
+    }
+  }
+  return true;
+}
+
+// state import, step 3 (on the device): the materialization predicate of every
+// live object, leading(o) = first position with no cached block of o
+// (P:614-618), one CTA per trace, positions marked in a shared window bitmap
+__global__ void derive_leading_kernel(PoolDev p, uint32_t trace_begin) {
+  constexpr uint32_t kWin = 1u << 15;   // positions per window (4 KB of bits)
+  __shared__ uint32_t bits[kWin / 32];
+  __shared__ uint32_t first_missing;
+  const size_t t = (size_t)trace_begin + blockIdx.x;
+  const uint32_t* meta = p.meta + t * p.NS;
+  uint2* obj = reinterpret_cast<uint2*>(p.obj) + t * p.O;
+  for (uint32_t o = 0; o < p.O; ++o) {
+    const uint32_t w0 = obj[o].x;
+    if (!obj_live(w0)) continue;
+    const uint32_t len = obj_len(w0);
+    uint32_t lead = len;
+    for (uint32_t w = 0; w < len; w += kWin) {
+      for (uint32_t i = threadIdx.x; i < kWin / 32; i += blockDim.x) bits[i] = 0;
+      if (threadIdx.x == 0) first_missing = 0xFFFFFFFFu;
+      __syncthreads();
+      for (uint32_t b = threadIdx.x; b < p.NS; b += blockDim.x) {
+        const uint32_t m = meta[b];
+        const uint32_t q = meta_pos(m);
+        if (meta_res(m) == kResCached && meta_owner(m) == o && q >= w && q < w + kWin)
+          atomicOr(&bits[(q - w) >> 5], 1u << ((q - w) & 31u));
+      }
+      __syncthreads();
+      const uint32_t span = min(kWin, len - w);
+      for (uint32_t q = threadIdx.x; q < span; q += blockDim.x)
+        if (!((bits[q >> 5] >> (q & 31u)) & 1u)) atomicMin(&first_missing, w + q);
+      __syncthreads();
+      const uint32_t fm = first_missing;
+      __syncthreads();
+      if (fm != 0xFFFFFFFFu) { lead = fm; break; }
+    }
+    if (threadIdx.x == 0) obj[o].y = lead;
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
 rkc_status rkc_state_import(rkc_pool* pool, uint32_t trace_begin, uint32_t n,
                             const rkc_header_view* headers, const rkc_block_view* blocks,
                             const rkc_claim_view* claims, const rkc_request_view* requests,
@@ -691,11 +812,21 @@ rkc_status rkc_state_import(rkc_pool* pool, uint32_t trace_begin, uint32_t n,
   if (!pool || !headers || !blocks || !claims || !requests || !objects ||
       trace_begin + (uint64_t)n > pool->d.num_traces)
     return RKC_E_INVAL;
+  if (n == 0) return RKC_OK;
+  RKC_ON_DEVICE(pool);
   const PoolDev& d = pool->d;
   const uint32_t N = pool->cfg.max_blocks, NS = d.NS;
   std::vector<uint32_t> hdr((size_t)n * H_NWORDS);
   CUDA_TRY(cudaDeviceSynchronize());
   CUDA_TRY(cudaMemcpy(hdr.data(), d.hdr + (size_t)trace_begin * H_NWORDS, hdr.size() * 4, cudaMemcpyDeviceToHost));
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t U = hdr[(size_t)i * H_NWORDS + H_U];
+    if (!views_valid(pool, U, blocks + (size_t)i * N, claims + (size_t)i * d.C,
+                     requests + (size_t)i * d.Q, objects + (size_t)i * d.O))
+      return RKC_E_INVAL;
+  }
+  // step 2 (host): block words with their selection keys, claim / request /
+  // object records, and the header counts
   std::vector<uint32_t> key((size_t)n * NS), meta((size_t)n * NS), fbm((size_t)n * NS / 32),
       clm((size_t)n * d.C * 8, 0), req((size_t)n * d.Q * 8, 0), obj((size_t)n * d.O * 2);
   for (uint32_t i = 0; i < n; ++i) {
@@ -705,14 +836,11 @@ rkc_status rkc_state_import(rkc_pool* pool, uint32_t trace_begin, uint32_t n,
     const rkc_claim_view* cv = claims + (size_t)i * d.C;
     const rkc_object_view* ov = objects + (size_t)i * d.O;
     const rkc_request_view* rv = requests + (size_t)i * d.Q;
-    std::vector<uint32_t> pc(d.C, 0), first_missing(d.O, 0xFFFFFFFFu), pin(d.O, 0);
-    std::vector<std::vector<uint8_t>> present(d.O);
+    std::vector<uint32_t> pc(d.C, 0), pin(d.O, 0);
     // pinned prefix per object: the longest hit of a running request (f3, G28)
     for (uint32_t r = 0; r < d.Q; ++r)
-      if (rv[r].status == R_RUNNING && rv[r].target < d.O)
-        pin[rv[r].target] = std::max(pin[rv[r].target], rv[r].hit);
+      if (rv[r].status == R_RUNNING) pin[rv[r].target] = std::max(pin[rv[r].target], rv[r].hit);
     uint32_t npinned = 0;
-    for (uint32_t o = 0; o < d.O; ++o) present[o].assign(ov[o].len, 0);
     uint32_t free_cnt = 0;
     for (uint32_t b = 0; b < NS; ++b) {
       const size_t k = (size_t)i * NS + b;
@@ -726,17 +854,15 @@ rkc_status rkc_state_import(rkc_pool* pool, uint32_t trace_begin, uint32_t n,
         meta[k] = meta_make(kResCached, v.owner, v.pos);
         uint32_t cls = 1;
         const uint32_t cc = ov[v.owner].claim;
-        const bool pinned = v.owner < d.O && v.pos < pin[v.owner];
-        if (pinned) {
+        if (v.pos < pin[v.owner]) {
           meta[k] |= kMetaPin;
           cls = 3;
           ++npinned;
         } else {
-          if (cc < 32 && live_state_h(cv[cc].state) && v.pos < cv[cc].F) cls = claim_class_h(cv[cc].mode, low);
+          if (cc < d.C && live_state_h(cv[cc].state) && v.pos < cv[cc].F) cls = claim_class_h(cv[cc].mode, low);
           if (cls == 3) pc[cc]++;
         }
         key[k] = (cls << kClassShift) | (v.seq & kSeqMask);
-        if (v.owner < d.O && v.pos < ov[v.owner].len) present[v.owner][v.pos] = 1;
       }
     }
     uint32_t P = 0, mask = 0, next_exp = 0xFFFFFFFFu, alive = 0;
@@ -761,10 +887,8 @@ rkc_status rkc_state_import(rkc_pool* pool, uint32_t trace_begin, uint32_t n,
     }
     alive += npinned;
     for (uint32_t o = 0; o < d.O; ++o) {
-      uint32_t lead = ov[o].len;
-      for (uint32_t q = 0; q < ov[o].len; ++q) if (!present[o][q]) { lead = q; break; }
       obj[((size_t)i * d.O + o) * 2] = obj_make(ov[o].live ? 1 : 0, ov[o].claim == 0xFF ? kNoClaim : ov[o].claim, ov[o].len);
-      obj[((size_t)i * d.O + o) * 2 + 1] = ov[o].live ? lead : 0;
+      obj[((size_t)i * d.O + o) * 2 + 1] = 0;   // leading: derived on the device below
     }
     h[H_SEQ] = headers[i].seq_ctr;
     h[H_FREE] = free_cnt;
@@ -780,6 +904,10 @@ rkc_status rkc_state_import(rkc_pool* pool, uint32_t trace_begin, uint32_t n,
   CUDA_TRY(cudaMemcpy(d.clm + (size_t)trace_begin * d.C * 8, clm.data(), clm.size() * 4, cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(d.req + (size_t)trace_begin * d.Q * 8, req.data(), req.size() * 4, cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(d.obj + (size_t)trace_begin * d.O * 2, obj.data(), obj.size() * 4, cudaMemcpyHostToDevice));
+  g_launches += 1;
+  derive_leading_kernel<<<n, 256>>>(d, trace_begin);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaDeviceSynchronize());
   return RKC_OK;
 }
 
@@ -802,6 +930,7 @@ rkc_status rkc_conformance_check(const rkc_event* events, const uint32_t* offset
 rkc_status rkc_pool_conformance(rkc_pool* pool, uint32_t* verdict_out, int64_t* evidence_out,
                                 void* stream) {
   if (!pool || !verdict_out) return RKC_E_INVAL;
+  RKC_ON_DEVICE(pool);
   CUDA_TRY(launch_conformance_pool(pool->d, verdict_out,
                                    reinterpret_cast<unsigned long long*>(evidence_out),
                                    (cudaStream_t)stream));

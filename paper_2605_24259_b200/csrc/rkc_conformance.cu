@@ -5,8 +5,9 @@
 // materialization, active conflict, blocking claims, and final outcome").
 //
 // Checks (a set bit in the per-trace verdict = the check FAILED):
-//   L1  every claim_harmed follows claim_accepted and claim_materialized of
-//       that claim ("no accepted claim, no claim harm")
+//   L1  every claim_harmed follows a claim_accepted of that claim ("no
+//       accepted claim, no claim harm"; "every claim_harmed
+//       event has an earlier claim_accepted for the same claim_id")
 //   L2  write no-admit is separate from allocation: every
 //       write_admission_denied is followed in the same step by
 //       request_served of the same request
@@ -20,9 +21,14 @@
 //   L6  predicate consistency: materialized => L >= R and tokens = 16 L;
 //       harmed => L < R; reuse probes report tokens = 16 L and
 //       satisfied = (bound claim live and L >= R)
-//   L7  lifecycle legality of the reconstruction and, when the final claim
-//       states are given, equality with them
-//   I4  under the contract lowering no obligated claim is harmed (north star)
+//   L7  lifecycle legality of the reconstruction (S:44 transitions, including
+//       accepted -> harmed) and, when the final claim states are given,
+//       equality with them
+//   I4  under the contract lowering no obligated claim is harmed (north star);
+//       checked only where the trace's lowering is known
+// A drained pool ring holds only the events after the drain: the checks then
+// start from "unknown" claim states and verify what the remaining events
+// determine (no final-state comparison).
 //   LOST the trace's event ring overflowed (checks ran on a prefix)
 #include <cuda_runtime.h>
 
@@ -42,17 +48,25 @@ struct EvIn {  // events of one trace: either a compacted array or a pool ring
   uint32_t n;
 };
 
+constexpr uint8_t kUnknown = 0xFE;    // claim state before a drained ring's first event
+constexpr uint32_t kNoLowering = 0xFF;  // lowering not given: I4 is not checked
+
+__device__ __forceinline__ bool live_or_unknown(uint8_t s) {
+  return s == C_ACCEPTED || s == C_MATERIALIZED || s == kUnknown;
+}
+
 __device__ uint32_t check_trace(const EvIn in, const uint8_t* final_states, uint32_t C,
-                                uint32_t lowering, bool lost, unsigned long long* ev_sum) {
+                                uint32_t lowering, bool lost, bool partial,
+                                unsigned long long* ev_sum) {
   uint8_t st[32];      // reconstructed claim states
   uint8_t rel[32];     // released (demoted / expired) before
-  uint8_t mat[32];     // materialized at some point
+  uint8_t acc[32];     // accepted at some point
   uint32_t R[32];      // claim threshold (from the accept record)
   uint8_t oc[128];     // object -> bound claim (0xFF none)
-  for (int i = 0; i < 32; ++i) { st[i] = 0; rel[i] = 0; mat[i] = 0; R[i] = 0; }
+  for (int i = 0; i < 32; ++i) { st[i] = partial ? kUnknown : 0; rel[i] = 0; acc[i] = 0; R[i] = 0; }
   for (int i = 0; i < 128; ++i) oc[i] = 0xFF;
   uint32_t fail = 0;
-  bool any_release = false;
+  bool any_release = partial;
   uint32_t pending_denied = 0xFFFFFFFFu, pending_step = 0;
   uint64_t e_acc = 0, e_mat = 0, e_harm = 0, e_ref = 0, e_att = 0, e_vic = 0, e_rel = 0, e_den = 0;
   for (uint32_t i = 0; i < in.n; ++i) {
@@ -65,26 +79,26 @@ __device__ uint32_t check_trace(const EvIn in, const uint8_t* final_states, uint
     }
     switch (type) {
       case EV_ACCEPTED:
-        if (slot >= C || st[slot] != C_EMPTY) { fail |= RKC_CHECK_L7; break; }
+        if (slot >= C || (st[slot] != C_EMPTY && st[slot] != kUnknown)) { fail |= RKC_CHECK_L7; break; }
         st[slot] = C_ACCEPTED;
+        acc[slot] = 1;
         R[slot] = f.z;
         if (f.x < 128) oc[f.x] = (uint8_t)slot;
         ++e_acc;
         break;
       case EV_REJECTED:
-        if (slot >= C || st[slot] != C_EMPTY) { fail |= RKC_CHECK_L7; break; }
+        if (slot >= C || (st[slot] != C_EMPTY && st[slot] != kUnknown)) { fail |= RKC_CHECK_L7; break; }
         st[slot] = C_REFUSED;
         break;
       case EV_MATERIALIZED:
-        if (slot >= C || st[slot] != C_ACCEPTED) { fail |= RKC_CHECK_L7; break; }
+        if (slot >= C || (st[slot] != C_ACCEPTED && st[slot] != kUnknown)) { fail |= RKC_CHECK_L7; break; }
         if (f.x < f.y || f.z != f.x * kBlockTokens) fail |= RKC_CHECK_L6;
         st[slot] = C_MATERIALIZED;
-        mat[slot] = 1;
         ++e_mat;
         break;
       case EV_DEMOTED:
       case EV_EXPIRED:
-        if (slot >= C || (st[slot] != C_ACCEPTED && st[slot] != C_MATERIALIZED)) {
+        if (slot >= C || !live_or_unknown(st[slot])) {
           fail |= RKC_CHECK_L7;
           break;
         }
@@ -94,9 +108,9 @@ __device__ uint32_t check_trace(const EvIn in, const uint8_t* final_states, uint
         break;
       case EV_HARMED:
         if (slot >= C) { fail |= RKC_CHECK_L7; break; }
-        if (st[slot] == C_EMPTY || !mat[slot]) fail |= RKC_CHECK_L1;
+        if (!acc[slot] && st[slot] != kUnknown) fail |= RKC_CHECK_L1;
         if (rel[slot]) fail |= RKC_CHECK_L45;
-        if (st[slot] != C_MATERIALIZED) fail |= RKC_CHECK_L7;
+        if (!live_or_unknown(st[slot])) fail |= RKC_CHECK_L7;
         if (f.x >= f.y) fail |= RKC_CHECK_L6;
         if (reason && lowering == LOW_CONTRACT) fail |= RKC_CHECK_I4;
         st[slot] = C_HARMED;
@@ -111,7 +125,7 @@ __device__ uint32_t check_trace(const EvIn in, const uint8_t* final_states, uint
         if ((reason == WHY_PROTECTED) != resident || (mask != 0) != resident) fail |= RKC_CHECK_L3;
         for (uint32_t c = 0; c < 32; ++c)
           if ((mask >> c) & 1u) {
-            if (c >= C || (st[c] != C_ACCEPTED && st[c] != C_MATERIALIZED)) fail |= RKC_CHECK_L3;
+            if (c >= C || !live_or_unknown(st[c])) fail |= RKC_CHECK_L3;
           }
         ++e_ref;
         if (mask) ++e_att;
@@ -130,10 +144,14 @@ __device__ uint32_t check_trace(const EvIn in, const uint8_t* final_states, uint
       case EV_REUSE_PROBE: {
         if (f.z != f.y * kBlockTokens) fail |= RKC_CHECK_L6;
         const uint32_t c = slot;
-        const bool live = c < C && (st[c] == C_ACCEPTED || st[c] == C_MATERIALIZED);
-        const bool sat = live && f.y >= R[c];
-        if ((reason != 0) != sat) fail |= RKC_CHECK_L6;
-        if (f.x >= 128 || oc[f.x] != c) fail |= RKC_CHECK_L7;  // probe names the bound claim
+        // what a drained ring cannot know: the bound claim and its threshold
+        const bool known = !partial || (f.x < 128 && oc[f.x] != 0xFF);
+        if (known) {
+          const bool live = c < C && (st[c] == C_ACCEPTED || st[c] == C_MATERIALIZED);
+          const bool sat = live && f.y >= R[c];
+          if ((reason != 0) != sat) fail |= RKC_CHECK_L6;
+          if (f.x >= 128 || oc[f.x] != c) fail |= RKC_CHECK_L7;  // probe names the bound claim
+        }
         break;
       }
       default:
@@ -167,7 +185,7 @@ __global__ void conformance_array_kernel(const uint4* ev, const uint32_t* offset
     const uint32_t b = offsets[t], e = offsets[t + 1];
     EvIn in{ev + (size_t)b * 2, e - b};
     verdict[t] = check_trace(in, final_states ? final_states + (size_t)t * C : nullptr, C,
-                             lowering ? lowering[t] : LOW_CONTRACT, false, evidence);
+                             lowering ? lowering[t] : kNoLowering, false, false, evidence);
     if (evidence) {
       const uint32_t f = verdict[t];
       if (f) atomicAdd(evidence + 8, 1ull);
@@ -183,8 +201,9 @@ __global__ void conformance_pool_kernel(PoolDev p, uint32_t* verdict, unsigned l
     for (uint32_t c = 0; c < p.C; ++c) fs[c] = (uint8_t)(p.clm[((size_t)t * p.C + c) * 8] & 0xFFu);
     const uint32_t low = p.hdr[(size_t)t * H_NWORDS + H_POLICY] & 0xFFu;
     // a drained or overflowed ring cannot be compared with the final states
-    const bool complete = ev <= p.EPT;
-    verdict[t] = check_trace(in, complete ? fs : nullptr, p.C, low, !complete, evidence);
+    const bool drained = p.hdr[(size_t)t * H_NWORDS + H_EVDRAINED] != 0;
+    const bool complete = ev <= p.EPT && !drained;
+    verdict[t] = check_trace(in, complete ? fs : nullptr, p.C, low, ev > p.EPT, drained, evidence);
     if (evidence && verdict[t]) atomicAdd(evidence + 8, 1ull);
   }
 }

@@ -80,11 +80,16 @@ enum : uint32_t { K_OPS = 0, K_ACCEPTED, K_REJECTED, K_MATERIALIZED, K_DEMOTED_E
                   K_REFUSED_PROTECTED, K_REFUSED_CAPACITY, K_INSERTED, K_INSERT_REFUSED,
                   K_WRITE_DENIED, K_VICTIMS_ORDINARY, K_VICTIMS_AFTER_RELEASE, K_VICTIMS_CLAIMED,
                   K_BLOCKS_ALLOCATED, K_BLOCKS_CACHED, K_REUSE_PROBES, K_REUSE_TOKENS,
-                  K_OP_ERRORS, K_STEPS, K_EVENTS, K_PREFIX_HITS, K_HIT_TOKENS, K_NCTR = 32 };
+                  K_OP_ERRORS, K_STEPS, K_EVENTS, K_PREFIX_HITS, K_HIT_TOKENS, K_ALLOCATIONS,
+                  K_NCTR = 32 };
 
 // hot header: 16 u32
 enum : uint32_t { H_U = 0, H_POLICY = 1, H_ACCEPT = 2, H_SEQ = 3, H_FREE = 4, H_ALIVE = 5,
-                  H_P = 6, H_BLOCKMASK = 7, H_NEXT_EXPIRY = 8, H_EVCOUNT = 9, H_NWORDS = 16 };
+                  H_P = 6, H_BLOCKMASK = 7, H_NEXT_EXPIRY = 8, H_EVCOUNT = 9, H_HOT = 10,
+                  H_EVDRAINED = 12, H_NWORDS = 16 };
+// words [0, H_HOT) are the hot header the step kernels carry and write back;
+// H_EVCOUNT counts the events in the trace's ring since the last drain,
+// H_EVDRAINED the events drained before it (host-side telemetry only)
 // H_POLICY bytes: lowering | admit_check << 8 | defer_budget << 16 | auto_demote << 24
 
 // claim record: 8 u32  (w0 = state | mode << 8 | obj << 16)

@@ -993,6 +993,7 @@ __device__ __noinline__ void alloc_free(uint32_t k, uint32_t owner, bool insert,
   crew_run(JOB_FREE_TAKE);
   hset(H_FREE, S.h[H_FREE] - k);
   ctr_add(K_BLOCKS_ALLOCATED, k);
+  ctr_add(K_ALLOCATIONS, 1);
   return;
 #endif
   uint32_t acc = 0;
@@ -1026,6 +1027,7 @@ __device__ __noinline__ void alloc_free(uint32_t k, uint32_t owner, bool insert,
   }
   hset(H_FREE, S.h[H_FREE] - k);
   ctr_add(K_BLOCKS_ALLOCATED, k);
+  ctr_add(K_ALLOCATIONS, 1);
 }
 
 // Evicting allocation (k > free count): every free block plus the k - free
@@ -1214,6 +1216,7 @@ __device__ __noinline__ void alloc_evict(uint32_t k, uint32_t owner, bool insert
   ctr_add(K_VICTIMS_AFTER_RELEASE, rel);
   ctr_add(K_VICTIMS_CLAIMED, clm);
   ctr_add(K_BLOCKS_ALLOCATED, k);
+  ctr_add(K_ALLOCATIONS, 1);
   if (ord + rel + clm > 0) {
     emit(EV_VICTIMS, owner, insert ? 1u : 0u, 0, ord, rel, clm, k);
     flag_set(F_POST);
@@ -1671,7 +1674,7 @@ __device__ __noinline__ void finish() {
     __syncwarp();
   }
   if (S.flags & F_HDR) {
-    if (lane_id() < H_NWORDS) S.hdrp[lane_id()] = S.h[lane_id()];
+    if (lane_id() < H_HOT) S.hdrp[lane_id()] = S.h[lane_id()];
   }
   __syncwarp();
   const uint32_t d = S.ctr[lane_id()];
@@ -1775,6 +1778,7 @@ __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_c
               rq[RQ_DONE] = done + n;
               atomicAdd(p.ctr + (size_t)t * K_NCTR + K_OPS, 1u);
               atomicAdd(p.ctr + (size_t)t * K_NCTR + K_BLOCKS_ALLOCATED, need);
+              atomicAdd(p.ctr + (size_t)t * K_NCTR + K_ALLOCATIONS, 1u);
               heavy = false;
             }
           }

@@ -65,7 +65,8 @@ def _load():
 def random_traces(config: int, seed: int, trace_begin: int, n_traces: int, T: int,
                   N: int, C: int = 16, Q: int = 16, O: int = 64, nthreads: int | None = None,
                   ops_out: np.ndarray | None = None):
-    """Random traces of recipe `config` (3 = c3/c5, 4 = c4, 6 = c3 + prefix hits).
+    """Random traces of recipe `config` (3 = c3/c5, 4 = c4, 6 = c3 + prefix hits,
+    7 = slot stress: every claim / request / object slot up to C, Q, O).
 
     Returns (cfgs[n_traces] CFG_DTYPE, ops[T, n_traces] OP_DTYPE).  ops_out
     may be a preallocated (e.g. pinned) uint8/OP_DTYPE buffer of T*n*16 bytes.

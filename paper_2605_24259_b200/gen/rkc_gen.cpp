@@ -89,7 +89,22 @@ struct Recipe {
  * demotion/expiry churn (configs[3]).  c5 = c3 recipe, 10^6 trace ids. */
 Recipe recipe(int config, uint32_t N) {
   Recipe r{};
-  if (config == 4) {
+  if (config == 7) {
+    /* c7 (parity only): slot stress -- every claim / request / object slot
+     * the pool allows (C, Q, O from the caller, up to 32 / 32 / 128), small
+     * objects and requests so that many coexist, hard-heavy claims so that
+     * refusals carry blocking masks over high claim slots */
+    r.U = N; r.C_lo = 32; r.C_hi = 32; r.Q = 32; r.O = 128;
+    r.insert_lo = std::max<uint32_t>(1, N / 64); r.insert_hi = std::max<uint32_t>(4, N / 12);
+    r.prompt_lo = 16; r.prompt_hi = std::max<uint32_t>(64, N * 4);
+    r.chunks[0] = 16; r.chunks[1] = 64; r.chunks[2] = 128; r.n_chunks = 3;
+    r.decode_hi = 32;
+    const double w[8] = {0.05, 0.14, 0.16, 0.35, 0.06, 0.12, 0.04, 0.08};
+    std::memcpy(r.op_w, w, sizeof w);
+    const double m[6] = {0.10, 0.45, 0.15, 0.10, 0.10, 0.10};
+    std::memcpy(r.mode_w, m, sizeof m);
+    r.exp_D_lo = 8; r.exp_D_hi = 64; r.D_lo = 8; r.D_hi = 128; r.D_zero = 0.7;
+  } else if (config == 4) {
     r.U = N; r.C_lo = 4; r.C_hi = 16; r.Q = 16; r.O = 128;
     r.insert_lo = 2048; r.insert_hi = 16384;
     r.prompt_lo = 8192; r.prompt_hi = 131072;
@@ -194,7 +209,7 @@ void gen_trace(int config, uint64_t seed, uint64_t trace_id, uint32_t T, uint32_
         if (r == Q) break;
         uint32_t prompt = g.uni(rc.prompt_lo, rc.prompt_hi);
         uint32_t chunk;
-        if (config == 4) chunk = rc.chunks[g.uni(0, 2)];
+        if (config == 4 || config == 7) chunk = rc.chunks[g.uni(0, 2)];
         else { const uint32_t ch[4] = {128, 256, 512, 1024}; chunk = ch[g.uni(0, 3)]; }
         uint32_t decode = g.uni(0, rc.decode_hi);
         if (config == 6 && !known_obj.empty() && g.bern(0.5)) {
@@ -262,13 +277,13 @@ void gen_trace(int config, uint64_t seed, uint64_t trace_id, uint32_t T, uint32_
 extern "C" {
 
 /* Generate n_traces random traces (trace ids trace_begin..trace_begin+n-1)
- * of T steps for recipe `config` (3 = c3/c5, 4 = c4) with pool size N and
+ * of T steps for recipe `config` (3 = c3/c5, 4 = c4, 6 = c6, 7 = slot stress) with pool size N and
  * slot limits C/Q/O.  cfg_out: [n] 12-byte configs; ops_out: [T][n] 16-byte
  * op records (step-major, the lockstep replay layout).  Returns 0. */
 int rkc_gen_random(int config, uint64_t seed, uint64_t trace_begin, uint32_t n_traces, uint32_t T,
                    uint32_t N, uint32_t C, uint32_t Q, uint32_t O, void* cfg_out, void* ops_out,
                    int nthreads) {
-  if (config != 3 && config != 4 && config != 6) return -1;
+  if (config != 3 && config != 4 && config != 6 && config != 7) return -1;
   Cfg* cfgs = (Cfg*)cfg_out;
   Op* ops = (Op*)ops_out;
   std::atomic<uint32_t> next{0};

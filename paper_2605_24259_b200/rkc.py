@@ -145,12 +145,15 @@ def _count(x, record_size: int) -> int:
     return nbytes // record_size
 
 
-def _stream(stream) -> int | None:
+def _stream(stream, device: int | None = None) -> int | None:
+    """A stream handle; None means torch's current stream on `device` (the
+    pool's device, so a pool on cuda:k is never driven from another device's
+    stream)."""
     if stream is None:
         try:
             import torch
             if torch.cuda.is_available():
-                return torch.cuda.current_stream().cuda_stream
+                return torch.cuda.current_stream(device).cuda_stream
         except Exception:
             pass
         return None
@@ -190,6 +193,9 @@ class Pool:
                "rkc_pool_create")
         self.handle = h
 
+    def _st(self, stream):
+        return _stream(stream, self.device)
+
     # -- lifecycle -----------------------------------------------------------
     def rkc_pool_destroy(self):
         if getattr(self, "handle", None):
@@ -205,7 +211,7 @@ class Pool:
             pass
 
     def rkc_pool_reset(self, stream=None):
-        _check(_lib.rkc_pool_reset(self.handle, _stream(stream)), "rkc_pool_reset")
+        _check(_lib.rkc_pool_reset(self.handle, self._st(stream)), "rkc_pool_reset")
 
     def rkc_pool_info(self):
         c = rkc_pool_config()
@@ -218,17 +224,17 @@ class Pool:
     def rkc_claim_submit(self, claims, stream=None):
         n = _count(claims, CLAIM_INPUT.itemsize)
         return _check(_lib.rkc_claim_submit(self.handle, _ptr(claims), n, _on_device(claims),
-                                            _stream(stream)), "rkc_claim_submit")
+                                            self._st(stream)), "rkc_claim_submit")
 
     def rkc_request_admit(self, reqs, stream=None):
         n = _count(reqs, REQUEST_INPUT.itemsize)
         return _check(_lib.rkc_request_admit(self.handle, _ptr(reqs), n, _on_device(reqs),
-                                             _stream(stream)), "rkc_request_admit")
+                                             self._st(stream)), "rkc_request_admit")
 
     def rkc_op_stage(self, ops, stream=None):
         n = _count(ops, TRACE_OP.itemsize)
         return _check(_lib.rkc_op_stage(self.handle, _ptr(ops), n, _on_device(ops),
-                                        _stream(stream)), "rkc_op_stage")
+                                        self._st(stream)), "rkc_op_stage")
 
     def rkc_staging_conflicts(self) -> int:
         v = _u64()
@@ -240,13 +246,13 @@ class Pool:
         """ops: None (run the staged step) or [S, num_traces] 16-byte op records
         (numpy host array, or a CUDA uint8/int tensor with S*num_traces*16 bytes)."""
         if ops is None:
-            return _check(_lib.rkc_step_batch(self.handle, None, 1, 0, _stream(stream)),
+            return _check(_lib.rkc_step_batch(self.handle, None, 1, 0, self._st(stream)),
                           "rkc_step_batch")
         if num_steps is None:
             nbytes = ops.nbytes if isinstance(ops, np.ndarray) else ops.numel() * ops.element_size()
             num_steps = nbytes // (16 * self.num_traces)
         return _check(_lib.rkc_step_batch(self.handle, _ptr(ops), int(num_steps), _on_device(ops),
-                                          _stream(stream)), "rkc_step_batch")
+                                          self._st(stream)), "rkc_step_batch")
 
     # -- telemetry -----------------------------------------------------------
     def rkc_telemetry_read(self, counters_out=None, events_out=None, hist_out=None, drain=False,
@@ -264,7 +270,7 @@ class Pool:
         written = _u64()
         st = _lib.rkc_telemetry_read(self.handle, _ptr(counters_out), _ptr(events_out), cap,
                                      ctypes.byref(written), _ptr(hist_out), on_dev,
-                                     1 if drain else 0, _stream(stream))
+                                     1 if drain else 0, self._st(stream))
         ok = (RKC_OK, RKC_E_LOST) if allow_lost else (RKC_OK,)
         _check(st, "rkc_telemetry_read", ok)
         return st, written.value
@@ -303,7 +309,7 @@ class Pool:
         import torch
         verdict = torch.zeros(self.num_traces, dtype=torch.int32, device=f"cuda:{self.device}")
         evidence = torch.zeros(RKC_NEVIDENCE, dtype=torch.int64, device=f"cuda:{self.device}")
-        _check(_lib.rkc_pool_conformance(self.handle, _ptr(verdict), _ptr(evidence), _stream(stream)),
+        _check(_lib.rkc_pool_conformance(self.handle, _ptr(verdict), _ptr(evidence), self._st(stream)),
                "rkc_pool_conformance")
         return verdict, evidence
 

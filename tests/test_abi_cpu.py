@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_binding_loads_and_matches_header():
     from paper_2605_24259_b200 import rkc
-    assert rkc.rkc_abi_version() == 1
+    assert rkc.rkc_abi_version() == 2
     assert set(rkc.EXPORTED_SYMBOLS) == set(_declared())
 
 

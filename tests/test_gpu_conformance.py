@@ -172,3 +172,38 @@ def test_faults_are_caught_by_the_right_check():
     assert _faulted(contract_harm)[0] & K["I4"]
     # and the unmodified streams pass
     assert (_faulted(lambda ev, fs: ev) == 0).all()
+
+
+def test_checker_equals_cpu_reconstruction():
+    """f2 parity: the GPU checker's per-trace verdicts and its
+    evidence vector equal the plain CPU reconstruction (oracle/conformance.py)
+    element by element -- on the GPU's own compacted streams of c3, c6 and c7
+    (slot stress) pools, with and without the lowering array, and on every
+    fault-injection stream (tests/test_oracle_conformance.py)."""
+    import torch
+    from oracle import conformance as cf
+    from paper_2605_24259_b200 import rkc
+    from test_oracle_conformance import faulted_streams
+    for recipe, N, C, O in [(3, 1024, 16, 64), (6, 1024, 16, 64), (7, 256, 32, 128)]:
+        cfgs, ops = gen.random_traces(recipe, 91, 0, 1500, 256, N, C, C, O)
+        pool = rkc.Pool(cfgs, N, C, C, O, events_per_trace=4 * 256 + 64)
+        pool.rkc_step_batch(torch.from_numpy(np.ascontiguousarray(ops).view(np.uint8).reshape(-1)).cuda(),
+                            256)
+        _, ev, _ = pool.read_all()
+        fs = pool.rkc_state_export()["claims"]["state"]
+        for low in (None, cfgs["lowering"]):
+            vg, eg = _check_array(ev, len(cfgs), fs, C=C, lowering=low)
+            vc, ec = cf.check_stream(ev, len(cfgs), C, fs, low)
+            assert (vg == vc).all() and (eg == ec).all(), (recipe, low is None)
+        # a stream with faults sprinkled in: the two still agree trace by trace
+        bad = ev.copy()
+        rng = np.random.default_rng(recipe)
+        pick = rng.choice(len(bad), size=min(300, len(bad)), replace=False)
+        bad["f"][pick, rng.integers(0, 4, size=len(pick))] += 1
+        vg, eg = _check_array(bad, len(cfgs), fs, C=C, lowering=cfgs["lowering"])
+        vc, ec = cf.check_stream(bad, len(cfgs), C, fs, cfgs["lowering"])
+        assert (vg == vc).all() and (eg == ec).all() and (vc != 0).sum() > 0
+    for name, ev, fs, low, check in faulted_streams():
+        vg, eg = _check_array(ev, 3, fs, lowering=low)
+        vc, ec = cf.check_stream(ev, 3, 16, fs, low)
+        assert (vg == vc).all() and (eg == ec).all(), name

@@ -80,6 +80,48 @@ def test_small_slot_limits_and_claim_slots_32():
     assert_parity(g, o, what="C32")
 
 
+@pytest.mark.parametrize("N", [256, 1536])
+def test_slot_stress_parity_all_slots(N):
+    """Recipe 7 (slot stress) on the o128 builds (small pools: keys staged in
+    shared memory; N > 1024: the crew kernel): claim slots up to 31, request
+    slots up to 31, object slots up to 127, refusals whose blocking masks carry
+    claim slots >= 16 (ballot masks, emit_lanes, mark_reclass_lanes on the
+    upper claim lanes)."""
+    cfgs, ops = gen.random_traces(7, seed=31 + N, trace_begin=0, n_traces=400, T=400, N=N,
+                                  C=32, Q=32, O=128)
+    k = ops["kind"]
+    assert ops["a"][k == gen.SUBMIT].max() == 31
+    assert ops["a"][(k == gen.ADMIT) | (k == gen.ADVANCE)].max() == 31
+    assert ops["a"][k == gen.INSERT].max() == 127
+    if N > 1024:     # big pools: usable sizes well below N keep the pressure on
+        cfgs["U"] = np.random.default_rng(N).integers(N // 6, N // 2, size=len(cfgs))
+    g = run_gpu(cfgs, ops, N=N, C=32, Q=32, O=128)
+    o = run_ref(cfgs, ops, N=N, C=32, Q=32, O=128)
+    assert_parity(g, o, what=f"slot stress N={N}")
+    ev = g["events"]
+    masks = ev["mask"][np.isin(ev["type"], [7, 8, 9])]
+    assert int(((masks >> 16) != 0).sum()) > 0
+    assert (g["requests"]["status"][:, 16:] != 0).any()
+    assert (g["claims"]["state"][:, 16:] != 0).any()
+    assert (g["objects"]["live"][:, 64:] != 0).any()
+
+
+def test_c4_full_length_parity():
+    """BASELINE configs[3] shape at full length: 32 traces x 1024 steps on
+    65536-block pools (the bench's c4 launch configuration: crew kernel, o128
+    build), with usable sizes drawn from [12000, 65536] so that refusals,
+    deferrals, insert refusals and harms occur at this size."""
+    cfgs, ops = gen.random_traces(4, seed=2, trace_begin=0, n_traces=32, T=1024, N=65536,
+                                  C=16, Q=16, O=128)
+    rng = np.random.default_rng(5)
+    cfgs["U"] = rng.integers(12000, 65537, size=len(cfgs))
+    g = run_gpu(cfgs, ops, N=65536, O=128)
+    o = run_ref(cfgs, ops, N=65536, O=128, nthreads=16)
+    assert_parity(g, o, what="c4 full length")
+    t = np.bincount(g["events"]["type"], minlength=16)
+    assert t[7] > 0 and t[8] > 0 and t[9] > 0 and t[6] > 0 and t[12] > 0
+
+
 def test_c4_subset_parity():
     cfgs, ops = gen.random_traces(4, seed=2, trace_begin=0, n_traces=4, T=64, N=65536,
                                   C=16, Q=16, O=128)
