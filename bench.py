@@ -547,6 +547,27 @@ def main():
     from paper_2605_24259_b200 import rkc
     host = bind_numa(gpu)
     dev = torch.device("cuda", gpu)
+    if os.environ.get("RKC_BENCH_WATCHDOG"):          # debugging: dump every stack if stuck
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["RKC_BENCH_WATCHDOG"]), exit=True)
+    gloo = dist_on and dist.get_backend() == "gloo"
+
+    def allreduce(t, op=None):
+        """SUM (or `op`) over ranks; gloo reduces a host copy (no gloo CUDA path)"""
+        if not dist_on:
+            return t
+        if gloo:
+            h = t.cpu()
+            if op is None:
+                allreduce_histogram(h)
+            else:
+                dist.all_reduce(h, op=op)
+            t.copy_(h)
+        elif op is None:
+            allreduce_histogram(t)
+        else:
+            dist.all_reduce(t, op=op)
+        return t
 
     # ---- inputs: this rank's shard, generated on the host, resident in HBM ----
     global TRACES
@@ -573,8 +594,7 @@ def main():
         if ev_pair is not None:
             ev_pair[1].record(stream)
         pool.rkc_telemetry_read(events_out=events_dev, hist_out=hist_dev, stream=stream)
-        if dist_on:
-            allreduce_histogram(hist_dev)
+        allreduce(hist_dev)
 
     _phase("pool created")
     for _ in range(args.warmup):
@@ -607,8 +627,7 @@ def main():
     ms = start.elapsed_time(stop)
     step_kernel_ms = sum(a.elapsed_time(b) for a, b in pairs)
     t = torch.tensor([ms, step_kernel_ms], dtype=torch.float64, device=dev)
-    if dist_on:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    allreduce(t, dist.ReduceOp.MAX)
     ms, step_kernel_ms = float(t[0]), float(t[1])
 
     _phase("timed region done")
@@ -636,13 +655,12 @@ def main():
                                 hist_out=hist_host, stream=stream)
         if dist_on:                                        # the histogram SUM over ranks
             hd = torch.from_numpy(hist_host).to(dev)
-            allreduce_histogram(hd)
+            allreduce(hd)
             hist_host[:] = hd.cpu().numpy()
         e1.record(stream)
         torch.cuda.synchronize()
         te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if dist_on:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        allreduce(te, dist.ReduceOp.MAX)
         return float(te[0])
 
     e2e_all = [e2e_pass() for _ in range(max(3, args.e2e_steps))]
@@ -682,8 +700,7 @@ def main():
     ab = algorithmic_bytes(ops, counters, events)
     tot = torch.tensor([non_nop, TRACES, len(events), sb["bytes"], ab["bytes"]],
                        dtype=torch.float64, device=dev)
-    if dist_on:
-        dist.all_reduce(tot)
+    allreduce(tot, dist.ReduceOp.SUM)
     total_events, total_traces, total_records = float(tot[0]), float(tot[1]), float(tot[2])
     survey_total, layout_total = float(tot[3]), float(tot[4])
 

@@ -84,13 +84,14 @@ enum { RKC_EV_CLAIM_ACCEPTED = 1, RKC_EV_CLAIM_REJECTED = 2, RKC_EV_CLAIM_MATERI
        RKC_EV_REUSE_PROBE = 13, RKC_EV_OP_ERROR = 14,
        RKC_EV_PREFIX_HIT = 15 /* slot = request; f = {object, h, 16h tokens, leading} */ };
 /* refusal reasons (G7) and OP_ERROR codes */
-enum { RKC_WHY_PROTECTED_RESIDENT = 1, RKC_WHY_ACTIVE_CAPACITY = 2 };
+enum { RKC_WHY_PROTECTED_RESIDENT = 1, RKC_WHY_ACTIVE_CAPACITY = 2,
+       RKC_WHY_RESIDENT_RESERVE = 3 /* admission under the resident reserve (f4) */ };
 enum { RKC_ERR_DUPLICATE_SLOT = 1, RKC_ERR_INVALID_ARG = 2, RKC_ERR_ILLEGAL_TRANSITION = 3,
        RKC_ERR_UNKNOWN_CLAIM = 4, RKC_ERR_UNKNOWN_REQUEST = 5, RKC_ERR_NO_CHUNKS_REMAINING = 6,
        RKC_ERR_OBJECT_IN_USE = 7, RKC_ERR_SEQ_EXHAUSTED = 8, RKC_ERR_UNKNOWN_OP = 9 };
 /* policy bytes */
 enum { RKC_LOWER_CONTRACT = 0, RKC_LOWER_SOFT = 1, RKC_LOWER_NATIVE = 2 };
-enum { RKC_ADMIT_PEAK = 0, RKC_ADMIT_NONE = 1 };
+enum { RKC_ADMIT_PEAK = 0, RKC_ADMIT_NONE = 1, RKC_ADMIT_RESERVE = 2 /* NEXT f4: resident reserve */ };
 enum { RKC_ACCEPT_CAPACITY = 0, RKC_ACCEPT_RESERVE = 1 };
 
 #define RKC_NCTR 32    /* per-trace u32 counters */

@@ -112,8 +112,9 @@ def check_trace(events, C: int, final_states=None, lowering=None, lost: bool = F
             P, A, U, short = f
             if P + A <= U or P + A - U != short:
                 fail |= L3
-            resident = A <= U and P > 0
-            if (reason == orc.WHY_PROTECTED_RESIDENT) != resident or (mask != 0) != resident:
+            resident = A <= U and P > 0    # P: protected blocks, or the reserve (f4, G34)
+            resident_reason = reason in (orc.WHY_PROTECTED_RESIDENT, orc.WHY_RESIDENT_RESERVE)
+            if resident_reason != resident or (mask != 0) != resident:
                 fail |= L3
             for c in range(32):
                 if mask >> c & 1 and (c >= C or st[c] not in LIVE):

@@ -56,7 +56,7 @@ EVENT_NAMES = {1: "claim_accepted", 2: "claim_rejected", 3: "claim_materialized"
 C_EMPTY, C_ACCEPTED, C_MATERIALIZED, C_DEMOTED, C_EXPIRED, C_REFUSED, C_HARMED = range(7)
 R_EMPTY, R_RUNNING, R_DEFERRED, R_REFUSED, R_COMPLETED = range(5)
 # reasons
-WHY_PROTECTED_RESIDENT, WHY_ACTIVE_CAPACITY = 1, 2
+WHY_PROTECTED_RESIDENT, WHY_ACTIVE_CAPACITY, WHY_RESIDENT_RESERVE = 1, 2, 3
 (ERR_DUPLICATE_SLOT, ERR_INVALID_ARG, ERR_ILLEGAL_TRANSITION, ERR_UNKNOWN_CLAIM,
  ERR_UNKNOWN_REQUEST, ERR_NO_CHUNKS_REMAINING, ERR_OBJECT_IN_USE, ERR_SEQ_EXHAUSTED,
  ERR_UNKNOWN_OP) = range(1, 10)
@@ -182,6 +182,7 @@ def render_refusal_json(ev, request_names: dict, claim_names: dict) -> dict:
     blocking = [claim_names[c] for c in range(32) if mask >> c & 1]
     P, A, U, short = (int(v) for v in ev["f"])
     feas = ("infeasible_preserve_resident_and_active" if ev["reason"] == WHY_PROTECTED_RESIDENT
+            else "infeasible_active_exceeds_reserve_headroom" if ev["reason"] == WHY_RESIDENT_RESERVE
             else "infeasible_active_exceeds_usable")
     return {
         "event": EVENT_NAMES[int(ev["type"])],

@@ -61,10 +61,10 @@ enum : uint8_t { ERR_DUPLICATE_SLOT = 1, ERR_INVALID_ARG = 2, ERR_ILLEGAL_TRANSI
 /* claim rejection reasons (G3, G15, G26) */
 enum : uint8_t { REJ_IDENTITY = 1, REJ_OBJECT_CLAIMED = 2, REJ_FOOTPRINT = 3, REJ_RESERVE = 4 };
 /* refusal / deferral reasons (G7) */
-enum : uint8_t { WHY_PROTECTED_RESIDENT = 1, WHY_ACTIVE_CAPACITY = 2 };
+enum : uint8_t { WHY_PROTECTED_RESIDENT = 1, WHY_ACTIVE_CAPACITY = 2, WHY_RESIDENT_RESERVE = 3 };
 /* policy bytes */
 enum : uint8_t { LOW_CONTRACT = 0, LOW_SOFT = 1, LOW_NATIVE = 2 };
-enum : uint8_t { ADMIT_PEAK = 0, ADMIT_NONE = 1 };
+enum : uint8_t { ADMIT_PEAK = 0, ADMIT_NONE = 1, ADMIT_RESERVE = 2 };
 enum : uint8_t { ACCEPT_CAPACITY = 0, ACCEPT_RESERVE = 1 };
 /* counters */
 enum { K_OPS = 0, K_ACCEPTED, K_REJECTED, K_MATERIALIZED, K_DEMOTED_EXPLICIT, K_DEMOTED_AUTO,
@@ -259,6 +259,28 @@ struct Trace {
       if (protected_of_claim(c) > 0) m |= 1u << c;
     return m;
   }
+  /* The resident reserve (NEXT f4): "Resident reserve -- Resident survives;
+   * active work that cannot fit is refused.  Modeled reserve action" (Table 5,
+   * P:573-574); "a static block count subtracted from usable headroom at
+   * admission; default reserve equals the sum of accepted hard-protected
+   * footprints".  Here: the footprints F of the live obligated claims when the
+   * contract lowering protects them, 0 otherwise (G34). */
+  uint64_t reserve_total() const {
+    if (cfg.lowering != LOW_CONTRACT) return 0;
+    uint64_t r = 0;
+    for (uint32_t c = 0; c < clm.size(); ++c)
+      if (live_claim(c) && obligated(clm[c].mode)) r += clm[c].F;
+    return r;
+  }
+  /* the claims holding the reserve, ascending slot (the attribution of a
+   * reserve refusal) */
+  uint32_t reserve_mask() const {
+    uint32_t m = 0;
+    if (cfg.lowering != LOW_CONTRACT) return 0;
+    for (uint32_t c = 0; c < clm.size(); ++c)
+      if (live_claim(c) && obligated(clm[c].mode)) m |= 1u << c;
+    return m;
+  }
   uint32_t count_res(uint8_t res) const {
     uint32_t n = 0;
     for (const Block& b : blk) n += b.res == res ? 1u : 0u;
@@ -312,10 +334,35 @@ struct Trace {
         return true;
       }
     }
-    const uint32_t shortfall = (uint32_t)((uint64_t)P + A - U);
     const bool resident_cause = (A <= U) && P > 0;
-    const uint8_t why = resident_cause ? WHY_PROTECTED_RESIDENT : WHY_ACTIVE_CAPACITY;
-    const uint32_t mask = resident_cause ? blocking_mask() : 0u;
+    return infeasible(resident_cause ? WHY_PROTECTED_RESIDENT : WHY_ACTIVE_CAPACITY,
+                      resident_cause ? blocking_mask() : 0u, P, A, requester, ins_obj);
+  }
+
+  /* admission under the resident reserve (admit_check = RESERVE, f4, G34):
+   * the request's active live footprint estimate must fit the headroom the
+   * reserve leaves, reserve + Alive + need <= U; otherwise the request is
+   * deferred or refused with reason RESIDENT_RESERVE, the reserving claims as
+   * the blocking set and the proof (reserve, A, U, reserve + A - U) -- or with
+   * ACTIVE_CAPACITY and no claims when A > U alone (G7).  No auto-demotion:
+   * the reserve is a static admission control. */
+  bool admit_reserve(uint32_t need, int requester) {
+    const uint64_t Rv = reserve_total();
+    const uint64_t A = (uint64_t)alive() + need;
+    if (Rv + A <= cfg.U) return true;
+    const bool resident_cause = (A <= cfg.U) && Rv > 0;
+    return infeasible(resident_cause ? WHY_RESIDENT_RESERVE : WHY_ACTIVE_CAPACITY,
+                      resident_cause ? reserve_mask() : 0u, (uint32_t)Rv, A, requester, 0);
+  }
+
+  /* the explicit active-side action on an infeasible boundary: an insert
+   * refusal (G17), or the request's deferral / refusal (G9) with the
+   * capacity proof (P, A, U, shortfall = P + A - U) and attribution */
+  bool infeasible(uint8_t why, uint32_t mask, uint32_t P, uint64_t A, int requester,
+                  uint32_t ins_obj) {
+    const uint32_t U = cfg.U;
+    const uint32_t shortfall = (uint32_t)((uint64_t)P + A - U);
+    const bool resident_cause = why != WHY_ACTIVE_CAPACITY;
     if (requester < 0) {
       emit(E_RESIDENT_INSERT_REFUSED, ins_obj, why, mask, P, (uint32_t)A, U, shortfall);
       ctr[K_INSERT_REFUSED]++;
@@ -432,6 +479,7 @@ struct Trace {
     q.prompt = op.x; q.chunk = op.y; q.decode = op.z; q.done = 0; q.live = 0; q.hit = 0;
     ctr[K_ADMITTED]++;
     if (cfg.admit_check == ADMIT_PEAK) arbitrate(peak_blocks(q), (int)r, 0); /* G8 */
+    else if (cfg.admit_check == ADMIT_RESERVE) admit_reserve(peak_blocks(q), (int)r);  /* f4 */
   }
 
   /* HIT_ADMIT (NEXT f3): admission of a request whose prompt begins with
@@ -467,6 +515,9 @@ struct Trace {
         if (is_protected(b)) newprot++;
       }
       if (!arbitrate(peak_blocks(q) - h + newpin - newprot, (int)r, 0)) return;
+    } else if (cfg.admit_check == ADMIT_RESERVE) {
+      /* f4: the exclusive part of the peak against the reserve (G34) */
+      if (!admit_reserve(peak_blocks(q) - h, (int)r)) return;
     }
     const uint32_t base = seq_ctr;
     for (Block& b : blk)
@@ -491,6 +542,7 @@ struct Trace {
     if (q.status == R_DEFERRED) {
       /* retry of a deferred request: re-run the admission check (G9) */
       if (cfg.admit_check == ADMIT_PEAK && !arbitrate(peak_blocks(q), (int)r, 0)) return;
+      if (cfg.admit_check == ADMIT_RESERVE && !admit_reserve(peak_blocks(q), (int)r)) return;
       q.status = R_RUNNING;
     }
     uint32_t n;

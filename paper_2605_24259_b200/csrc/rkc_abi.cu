@@ -398,7 +398,7 @@ rkc_status rkc_pool_create(const rkc_pool_config* config, const rkc_trace_config
   for (uint32_t t = 0; t < c.num_traces; ++t) {
     const rkc_trace_config& tc = per_trace[t];
     if (tc.usable_blocks < 1 || tc.usable_blocks > c.max_blocks || tc.lowering > 2 ||
-        tc.admit_check > 1 || tc.auto_demote > 1 || tc.accept_rule > 1)
+        tc.admit_check > 2 || tc.auto_demote > 1 || tc.accept_rule > 1)
       return RKC_E_INVAL;
   }
   int ndev = 0;

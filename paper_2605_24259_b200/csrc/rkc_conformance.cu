@@ -63,7 +63,8 @@ __device__ uint32_t check_trace(const EvIn in, const uint8_t* final_states, uint
   uint8_t acc[32];     // accepted at some point
   uint32_t R[32];      // claim threshold (from the accept record)
   uint8_t oc[128];     // object -> bound claim (0xFF none)
-  for (int i = 0; i < 32; ++i) { st[i] = partial ? kUnknown : 0; rel[i] = 0; acc[i] = 0; R[i] = 0; }
+  // (a drained ring's claims may have been accepted before the drain)
+  for (int i = 0; i < 32; ++i) { st[i] = partial ? kUnknown : 0; rel[i] = 0; acc[i] = partial; R[i] = 0; }
   for (int i = 0; i < 128; ++i) oc[i] = 0xFF;
   uint32_t fail = 0;
   bool any_release = partial;
@@ -121,8 +122,9 @@ __device__ uint32_t check_trace(const EvIn in, const uint8_t* final_states, uint
       case EV_INSERT_REFUSED: {
         const uint64_t P = f.x, A = f.y, U = f.z;
         if (P + A <= U || P + A - U != f.w) fail |= RKC_CHECK_L3;
-        const bool resident = A <= U && P > 0;
-        if ((reason == WHY_PROTECTED) != resident || (mask != 0) != resident) fail |= RKC_CHECK_L3;
+        const bool resident = A <= U && P > 0;  // P: protected blocks, or the reserve (f4)
+        const bool resident_reason = reason == WHY_PROTECTED || reason == WHY_RESERVE;
+        if (resident_reason != resident || (mask != 0) != resident) fail |= RKC_CHECK_L3;
         for (uint32_t c = 0; c < 32; ++c)
           if ((mask >> c) & 1u) {
             if (c >= C || !live_or_unknown(st[c])) fail |= RKC_CHECK_L3;

@@ -70,9 +70,9 @@ enum : uint32_t { ERR_DUPLICATE_SLOT = 1, ERR_INVALID_ARG = 2, ERR_ILLEGAL_TRANS
                   ERR_UNKNOWN_CLAIM = 4, ERR_UNKNOWN_REQUEST = 5, ERR_NO_CHUNKS = 6,
                   ERR_OBJECT_IN_USE = 7, ERR_SEQ_EXHAUSTED = 8, ERR_UNKNOWN_OP = 9 };
 enum : uint32_t { REJ_IDENTITY = 1, REJ_OBJECT_CLAIMED = 2, REJ_FOOTPRINT = 3, REJ_RESERVE = 4 };
-enum : uint32_t { WHY_PROTECTED = 1, WHY_CAPACITY = 2 };
+enum : uint32_t { WHY_PROTECTED = 1, WHY_CAPACITY = 2, WHY_RESERVE = 3 };
 enum : uint32_t { LOW_CONTRACT = 0, LOW_SOFT = 1, LOW_NATIVE = 2 };
-enum : uint32_t { ADMIT_PEAK = 0, ADMIT_NONE = 1 };
+enum : uint32_t { ADMIT_PEAK = 0, ADMIT_NONE = 1, ADMIT_RESERVE = 2 };
 enum : uint32_t { ACCEPT_CAPACITY = 0, ACCEPT_RESERVE = 1 };
 enum : uint32_t { K_OPS = 0, K_ACCEPTED, K_REJECTED, K_MATERIALIZED, K_DEMOTED_EXPLICIT,
                   K_DEMOTED_AUTO, K_EXPIRED, K_HARMED_OBLIGATED, K_HARMED_UNOBLIGATED,

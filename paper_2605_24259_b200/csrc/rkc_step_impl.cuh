@@ -859,6 +859,61 @@ __device__ __noinline__ void drop_request_kv(uint32_t r) {
 }
 
 // ------------------------------ arbiter ------------------------------------
+// The explicit active-side action on an infeasible boundary: an insert
+// refusal (G17), or the request's deferral / refusal (G9), with the capacity
+// proof (P, A, U, shortfall = P + A - U) and the blocking claims.
+__device__ __noinline__ bool infeasible(uint32_t why, uint32_t mask, uint32_t P, uint64_t A,
+                                        uint32_t requester, uint32_t obj) {
+  const uint32_t U = S.h[H_U];
+  const uint32_t pol = S.h[H_POLICY];
+  const uint32_t shortfall = (uint32_t)((uint64_t)P + A - U);
+  const bool resident = why != WHY_CAPACITY;
+  if (requester == 0xFFFFFFFFu) {
+    emit(EV_INSERT_REFUSED, obj, why, mask, P, (uint32_t)A, U, shortfall);
+    ctr_add(K_INSERT_REFUSED, 1);
+    return false;
+  }
+  // request: release its live blocks, then defer or refuse (G9)
+  drop_request_kv(requester);
+  const uint32_t w0 = S.rq[RQ_W0];
+  const uint32_t defer = w0 >> 24;
+  const bool dfr = defer < ((pol >> 16) & 0xFFu);
+  __syncwarp();
+  if (lane_id() == 0) {
+    S.rq[RQ_LIVE] = 0;
+    S.rq[RQ_DONE] = 0;
+    S.rq[RQ_W0] = dfr ? ((w0 & 0x00FFFF00u) | R_DEFERRED | ((defer + 1) << 24))
+                       : ((w0 & 0xFFFFFF00u) | R_REFUSED);
+  }
+  __syncwarp();
+  if (dfr) {
+    emit(EV_DEFERRED, requester, why, mask, P, (uint32_t)A, U, shortfall);
+    ctr_add(resident ? K_DEFERRED_PROTECTED : K_DEFERRED_CAPACITY, 1);
+  } else {
+    emit(EV_REFUSED, requester, why, mask, P, (uint32_t)A, U, shortfall);
+    ctr_add(resident ? K_REFUSED_PROTECTED : K_REFUSED_CAPACITY, 1);
+  }
+  return false;
+}
+
+// Admission under the resident reserve (admit_check = RESERVE, NEXT f4, G34;
+// Table 5 "Resident reserve"): reserve = F summed over the
+// live obligated claims under the contract lowering (lane = claim slot);
+// the request is admitted iff reserve + Alive + need <= U, else deferred or
+// refused with the reserving claims as the blocking set.  No auto-demotion.
+__device__ __noinline__ bool admit_reserve(uint32_t need, uint32_t requester) {
+  need_claims();
+  const uint32_t U = S.h[H_U];
+  const bool res = lowering() == LOW_CONTRACT && lane_id() < S.C &&
+                   live_state(cl_state(lane_id())) && obligated(cl_mode(lane_id()));
+  const uint32_t Rv = __reduce_add_sync(kFull, res ? S.cl[lane_id()][CF_F] : 0u);
+  const uint32_t mask = __ballot_sync(kFull, res);
+  const uint64_t A = (uint64_t)S.h[H_ALIVE] + need;
+  if ((uint64_t)Rv + A <= U) return true;
+  const bool resident = A <= U && Rv > 0;
+  return infeasible(resident ? WHY_RESERVE : WHY_CAPACITY, resident ? mask : 0u, Rv, A, requester, 0);
+}
+
 // Feasibility boundary protected + active <= usable; relax by
 // auto-demotion (G10); else explicit refusal / deferral with
 // blocking-claim attribution and the capacity proof.
@@ -892,36 +947,9 @@ __device__ __noinline__ bool arbitrate(uint32_t need, uint32_t requester, uint32
       return true;
     }
   }
-  const uint32_t shortfall = (uint32_t)((uint64_t)P + A - U);
   const bool resident = A <= U && P > 0;
-  const uint32_t why = resident ? WHY_PROTECTED : WHY_CAPACITY;
-  const uint32_t mask = resident ? S.h[H_BLOCKMASK] : 0u;
-  if (requester == 0xFFFFFFFFu) {
-    emit(EV_INSERT_REFUSED, obj, why, mask, P, (uint32_t)A, U, shortfall);
-    ctr_add(K_INSERT_REFUSED, 1);
-    return false;
-  }
-  // request: release its live blocks, then defer or refuse (G9)
-  drop_request_kv(requester);
-  const uint32_t w0 = S.rq[RQ_W0];
-  const uint32_t defer = w0 >> 24;
-  const bool dfr = defer < ((pol >> 16) & 0xFFu);
-  __syncwarp();
-  if (lane_id() == 0) {
-    S.rq[RQ_LIVE] = 0;
-    S.rq[RQ_DONE] = 0;
-    S.rq[RQ_W0] = dfr ? ((w0 & 0x00FFFF00u) | R_DEFERRED | ((defer + 1) << 24))
-                       : ((w0 & 0xFFFFFF00u) | R_REFUSED);
-  }
-  __syncwarp();
-  if (dfr) {
-    emit(EV_DEFERRED, requester, why, mask, P, (uint32_t)A, U, shortfall);
-    ctr_add(resident ? K_DEFERRED_PROTECTED : K_DEFERRED_CAPACITY, 1);
-  } else {
-    emit(EV_REFUSED, requester, why, mask, P, (uint32_t)A, U, shortfall);
-    ctr_add(resident ? K_REFUSED_PROTECTED : K_REFUSED_CAPACITY, 1);
-  }
-  return false;
+  return infeasible(resident ? WHY_PROTECTED : WHY_CAPACITY, resident ? S.h[H_BLOCKMASK] : 0u, P, A,
+                    requester, obj);
 }
 
 // ------------------------------ victim selection ---------------------------
@@ -1307,7 +1335,9 @@ __device__ __noinline__ void op_admit(const Op op) {
   }
   __syncwarp();
   ctr_add(K_ADMITTED, 1);
-  if (((S.h[H_POLICY] >> 8) & 0xFFu) == ADMIT_PEAK) arbitrate(peak_blocks(), op.a, 0);
+  const uint32_t chk = (S.h[H_POLICY] >> 8) & 0xFFu;
+  if (chk == ADMIT_PEAK) arbitrate(peak_blocks(), op.a, 0);
+  else if (chk == ADMIT_RESERVE) admit_reserve(peak_blocks(), op.a);
   store_request(op.a);
 }
 
@@ -1347,6 +1377,11 @@ __device__ __noinline__ void op_hit_admit(const Op op) {
       store_request(op.a);
       return;
     }
+  } else if (((S.h[H_POLICY] >> 8) & 0xFFu) == ADMIT_RESERVE) {
+    if (!admit_reserve(peak_blocks() - h, op.a)) {  // f4: the exclusive part of the peak (G34)
+      store_request(op.a);
+      return;
+    }
   }
   if (h > 0) {
     const uint32_t seq_base = S.h[H_SEQ];
@@ -1378,7 +1413,9 @@ __device__ __noinline__ void op_advance(const Op op) {
   if (st == R_RUNNING && (uint64_t)S.rq[RQ_DONE] >= (uint64_t)S.rq[RQ_PROMPT] + S.rq[RQ_DECODE])
     return op_error(op, ERR_NO_CHUNKS);
   if (st == R_DEFERRED) {
-    if (((S.h[H_POLICY] >> 8) & 0xFFu) == ADMIT_PEAK && !arbitrate(peak_blocks(), op.a, 0)) {
+    const uint32_t chk = (S.h[H_POLICY] >> 8) & 0xFFu;
+    if ((chk == ADMIT_PEAK && !arbitrate(peak_blocks(), op.a, 0)) ||
+        (chk == ADMIT_RESERVE && !admit_reserve(peak_blocks(), op.a))) {
       store_request(op.a);
       return;
     }
@@ -1789,8 +1826,8 @@ __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_c
         const uint32_t status = __ldcg(rq) & 0xFFu;
         if (step < nexp && status != R_RUNNING && status != R_DEFERRED) {
           const uint64_t peak = ((uint64_t)opw.y + opw.w + kBlockTokens - 1) / kBlockTokens;
-          const bool peak_check = ((hv0.y >> 8) & 0xFFu) == ADMIT_PEAK;
-          if (!peak_check || (uint64_t)hv1.z + hv1.y + peak <= hv0.x) {
+          const uint32_t chk = (hv0.y >> 8) & 0xFFu;  // RESERVE admissions take the warp path
+          if (chk == ADMIT_NONE || (chk == ADMIT_PEAK && (uint64_t)hv1.z + hv1.y + peak <= hv0.x)) {
             reinterpret_cast<uint4*>(rq)[0] =
                 make_uint4(R_RUNNING | ((opw.x >> 24) << 8) | (((opw.x >> 16) & 0xFFu) << 16), opw.y,
                            opw.z, opw.w);

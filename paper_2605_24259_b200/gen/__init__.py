@@ -30,7 +30,7 @@ NOP, SUBMIT, ADMIT, ADVANCE, COMPLETE, INSERT, DEMOTE, TOUCH, HIT_ADMIT = range(
 SOFT, HARD, DEMOTABLE, OFFLOADABLE, EXPIRING, BEST_EFFORT = range(6)
 # policy bytes
 CONTRACT, SOFT_LOWERING, NATIVE = 0, 1, 2
-PEAK, NONE = 0, 1
+PEAK, NONE, ADMIT_RESERVE = 0, 1, 2     # admit_check (ADMIT_RESERVE: NEXT f4)
 CAPACITY, RESERVE = 0, 1
 ID_MISMATCH = 0x80
 
@@ -66,7 +66,8 @@ def random_traces(config: int, seed: int, trace_begin: int, n_traces: int, T: in
                   N: int, C: int = 16, Q: int = 16, O: int = 64, nthreads: int | None = None,
                   ops_out: np.ndarray | None = None):
     """Random traces of recipe `config` (3 = c3/c5, 4 = c4, 6 = c3 + prefix hits,
-    7 = slot stress: every claim / request / object slot up to C, Q, O).
+    7 = slot stress: every claim / request / object slot up to C, Q, O; 8 = c3 with
+    resident-reserve admission (NEXT f4) on 40 % of the traces).
 
     Returns (cfgs[n_traces] CFG_DTYPE, ops[T, n_traces] OP_DTYPE).  ops_out
     may be a preallocated (e.g. pinned) uint8/OP_DTYPE buffer of T*n*16 bytes.

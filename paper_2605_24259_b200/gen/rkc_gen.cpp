@@ -140,7 +140,12 @@ void gen_trace(int config, uint64_t seed, uint64_t trace_id, uint32_t T, uint32_
   Cfg cfg{};
   cfg.U = rc.U;
   { const double w[3] = {0.70, 0.15, 0.15}; cfg.lowering = (uint8_t)g.pick(w); }
-  cfg.admit_check = g.bern(0.8) ? 0 : 1;
+  if (config == 8) {  /* c8 (NEXT f4): c3 with resident-reserve admission on 40 % of the traces */
+    const double w[3] = {0.40, 0.20, 0.40};
+    cfg.admit_check = (uint8_t)g.pick(w);
+  } else {
+    cfg.admit_check = g.bern(0.8) ? 0 : 1;
+  }
   cfg.defer_budget = (uint8_t)g.uni(0, 2);
   cfg.auto_demote = g.bern(0.5) ? 1 : 0;
   cfg.accept_rule = g.bern(0.8) ? 0 : 1;
@@ -277,13 +282,14 @@ void gen_trace(int config, uint64_t seed, uint64_t trace_id, uint32_t T, uint32_
 extern "C" {
 
 /* Generate n_traces random traces (trace ids trace_begin..trace_begin+n-1)
- * of T steps for recipe `config` (3 = c3/c5, 4 = c4, 6 = c6, 7 = slot stress) with pool size N and
+ * of T steps for recipe `config` (3 = c3/c5, 4 = c4, 6 = c6, 7 = slot stress, 8 = c3 with
+ * resident-reserve admission) with pool size N and
  * slot limits C/Q/O.  cfg_out: [n] 12-byte configs; ops_out: [T][n] 16-byte
  * op records (step-major, the lockstep replay layout).  Returns 0. */
 int rkc_gen_random(int config, uint64_t seed, uint64_t trace_begin, uint32_t n_traces, uint32_t T,
                    uint32_t N, uint32_t C, uint32_t Q, uint32_t O, void* cfg_out, void* ops_out,
                    int nthreads) {
-  if (config != 3 && config != 4 && config != 6 && config != 7) return -1;
+  if (config != 3 && config != 4 && config != 6 && config != 7 && config != 8) return -1;
   Cfg* cfgs = (Cfg*)cfg_out;
   Op* ops = (Op*)ops_out;
   std::atomic<uint32_t> next{0};

@@ -92,7 +92,7 @@ def test_slot_stress_parity_all_slots(N):
     k = ops["kind"]
     assert ops["a"][k == gen.SUBMIT].max() == 31
     assert ops["a"][(k == gen.ADMIT) | (k == gen.ADVANCE)].max() == 31
-    assert ops["a"][k == gen.INSERT].max() == 127
+    assert max(ops["a"][k == gen.INSERT].max(), ops["b"][k == gen.ADMIT].max()) == 127
     if N > 1024:     # big pools: usable sizes well below N keep the pressure on
         cfgs["U"] = np.random.default_rng(N).integers(N // 6, N // 2, size=len(cfgs))
     g = run_gpu(cfgs, ops, N=N, C=32, Q=32, O=128)
@@ -304,3 +304,31 @@ def test_histogram_shard_invariance():
     s = a + b
     assert (np.delete(s, steps) == np.delete(whole, steps)).all()
     assert s[steps] == whole[steps]
+
+
+def test_reserve_admission_parity():
+    """NEXT f4 (resident-reserve admission, G34): the c8 recipe (c3 with
+    admit_check = RESERVE on 40 % of the traces) and the hand-built reserve
+    cases of tests/test_oracle_reserve.py, GPU = oracle bit for bit."""
+    from paper_2605_24259_b200.gen import (ADMIT, ADMIT_RESERVE, ADVANCE, CONTRACT, DEMOTE, HARD,
+                                           HIT_ADMIT, INSERT, SUBMIT, make_cfg, op, pack_ops)
+    cfgs, ops = gen.random_traces(8, seed=17, trace_begin=0, n_traces=2000, T=256, N=1024)
+    g = run_gpu(cfgs, ops, N=1024)
+    o = run_ref(cfgs, ops, N=1024)
+    assert_parity(g, o, what="c8")
+    ev = g["events"]
+    assert ((ev["type"] == orc.E_ACTIVE_REFUSED) & (ev["reason"] == orc.WHY_RESIDENT_RESERVE)).sum() > 0
+    lists = [
+        [op(INSERT, 0, x=40), op(SUBMIT, 0, 0, HARD, 60, 40, 0), op(ADMIT, 0, 1, 0, 656, 656, 0)],
+        [op(SUBMIT, 0, 0, HARD, 60, 60, 0), op(ADMIT, 0, 1, 0, 1120, 1120, 0), op(ADVANCE, 0),
+         op(INSERT, 0, x=60)],
+        [op(SUBMIT, 0, 0, HARD, 50, 1, 0), op(ADMIT, 0, 1, 0, 640, 640, 0), op(DEMOTE, 0),
+         op(ADVANCE, 0)],
+        [op(INSERT, 0, x=30), op(SUBMIT, 0, 0, HARD, 30, 30, 0),
+         op(HIT_ADMIT, 0, 0, 0, 16 * 60, 64, 0), op(ADVANCE, 0)],
+    ]
+    cf = np.stack([make_cfg(100, CONTRACT, ADMIT_RESERVE), make_cfg(80, CONTRACT, ADMIT_RESERVE),
+                   make_cfg(80, CONTRACT, ADMIT_RESERVE, defer_budget=1),
+                   make_cfg(80, CONTRACT, ADMIT_RESERVE)])
+    ops2 = pack_ops(lists)
+    assert_parity(run_gpu(cf, ops2, N=100), run_ref(cf, ops2, N=100), what="reserve cases")

@@ -21,7 +21,10 @@ def main(path, out, source):
         v = float(row[col[name]].replace(",", ""))
         u = units[col[name]]
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3,
-                 "usecond": 1, "msecond": 1e3}.get(u, 1)
+                 "usecond": 1, "msecond": 1e3, "ns": 1e-3, "us": 1, "ms": 1e3, "inst": 1, "": 1}
+        if u not in scale:
+            raise ValueError(f"unknown unit {u!r} for {name}")
+        scale = scale[u]
         return v * scale
 
     for row in rows[2:]:

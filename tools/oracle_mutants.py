@@ -18,7 +18,7 @@ LIB = os.path.join(ROOT, "oracle", "librkc_oracle.so")
 TESTS = ["tests/test_oracle_decisions.py", "tests/test_oracle_paper.py",
          "tests/test_oracle_litmus.py", "tests/test_oracle_bruteforce.py",
          "tests/test_oracle_prefix_hits.py", "tests/test_oracle_random.py",
-         "tests/test_oracle_reconstruct.py"]
+         "tests/test_oracle_reserve.py", "tests/test_oracle_conformance.py"]
 
 # (name, old, new): each `old` must occur exactly once in the oracle source
 MUTANTS = [
@@ -50,6 +50,14 @@ MUTANTS = [
      "return c != NO_OBJ_CLAIM && live_claim(c);"),
     ("mask kept when A > U", "const bool resident_cause = (A <= U) && P > 0;",
      "const bool resident_cause = P > 0;"),
+    ("admission reserve counts non-obligated claims",
+     "      if (live_claim(c) && obligated(clm[c].mode)) r += clm[c].F;",
+     "      if (live_claim(c)) r += clm[c].F;"),
+    ("admission reserve = cached protected blocks", "    const uint64_t Rv = reserve_total();",
+     "    const uint64_t Rv = protected_total();"),
+    ("admission reserve under every lowering", "    if (cfg.lowering != LOW_CONTRACT) return 0;\n    uint64_t r = 0;",
+     "    uint64_t r = 0;"),
+    ("admission reserve boundary <", "    if (Rv + A <= cfg.U) return true;", "    if (Rv + A < cfg.U) return true;"),
     ("shortfall off by one", "const uint32_t shortfall = (uint32_t)((uint64_t)P + A - U);",
      "const uint32_t shortfall = (uint32_t)((uint64_t)P + A - U - 1);"),
 ]
