@@ -56,6 +56,8 @@ struct rkc_pool {
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
   uint4* replay_buf[2] = {nullptr, nullptr};
+  void* scratch = nullptr;       // grow-only device staging for host-side telemetry outputs
+  size_t scratch_bytes = 0;
   size_t replay_steps = 0;       // steps per replay staging buffer
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr};
@@ -310,11 +312,30 @@ rkc_status run_init(rkc_pool* p, cudaStream_t st) {
 void free_all(rkc_pool* p) {
   for (void* a : p->allocs) cudaFree(a);
   p->allocs.clear();
+  if (p->scratch) cudaFree(p->scratch);
+  p->scratch = nullptr;
+  p->scratch_bytes = 0;
   for (int i = 0; i < 2; ++i) {
     if (p->ev_copied[i]) cudaEventDestroy(p->ev_copied[i]);
     if (p->ev_free[i]) cudaEventDestroy(p->ev_free[i]);
   }
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+}
+
+// device staging for host outputs of rkc_telemetry_read: kept across calls
+// (grown when a read needs more), so a host read costs the gather and the
+// copy, not an allocation and a mapping of gigabytes every time
+rkc_status scratch_for(rkc_pool* p, size_t bytes, cudaStream_t st, void** out) {
+  if (bytes > p->scratch_bytes) {
+    if (cudaStreamSynchronize(st) != cudaSuccess) return RKC_E_CUDA;
+    if (p->scratch) cudaFree(p->scratch);
+    p->scratch = nullptr;
+    p->scratch_bytes = 0;
+    if (cudaMalloc(&p->scratch, bytes) != cudaSuccess) { cudaGetLastError(); return RKC_E_NOMEM; }
+    p->scratch_bytes = bytes;
+  }
+  *out = p->scratch;
+  return RKC_OK;
 }
 
 // stage n converted ops (device) via the conflict-resolving commit
@@ -605,28 +626,28 @@ rkc_status rkc_telemetry_read(rkc_pool* pool, uint32_t* counters_out, rkc_event*
   CUDA_TRY(cudaStreamSynchronize(st));
   if (events_written) *events_written = host_total;
   if (events_out && host_total > events_cap) return RKC_E_OVERFLOW;
-  if (events_out && host_total > 0) {
-    uint4* dst = nullptr;
-    if (on_device) dst = reinterpret_cast<uint4*>(events_out);
-    else CUDA_TRY(cudaMallocAsync(&dst, (size_t)host_total * 32, st));
+  // host outputs: staged in the pool's grow-only scratch, events first, then counters
+  const size_t ev_bytes = (events_out && host_total > 0) ? (size_t)host_total * 32 : 0;
+  const size_t ctr_bytes = counters_out ? T * K_NCTR * 4 : 0;
+  char* stage = nullptr;
+  if (!on_device && ev_bytes + ctr_bytes > 0) {
+    rkc_status s = scratch_for(pool, ev_bytes + ctr_bytes, st, (void**)&stage);
+    if (s != RKC_OK) return s;
+  }
+  if (ev_bytes) {
+    uint4* dst = on_device ? reinterpret_cast<uint4*>(events_out) : reinterpret_cast<uint4*>(stage);
     g_launches += 1;
     event_gather_kernel<<<grid_for(T * 32), kThreads, 0, st>>>(d, pool->counts, pool->offsets, dst);
     CUDA_TRY(cudaGetLastError());
-    if (!on_device) {
-      CUDA_TRY(cudaMemcpyAsync(events_out, dst, (size_t)host_total * 32, cudaMemcpyDeviceToHost, st));
-      cudaFreeAsync(dst, st);
-    }
+    if (!on_device)
+      CUDA_TRY(cudaMemcpyAsync(events_out, dst, ev_bytes, cudaMemcpyDeviceToHost, st));
   }
   if (counters_out) {
-    uint32_t* dst = nullptr;
-    if (on_device) dst = counters_out;
-    else CUDA_TRY(cudaMallocAsync(&dst, T * K_NCTR * 4, st));
+    uint32_t* dst = on_device ? counters_out : reinterpret_cast<uint32_t*>(stage + ev_bytes);
     g_launches += 1;
     counters_kernel<<<grid_for(T * K_NCTR), kThreads, 0, st>>>(d, pool->step, dst);
-    if (!on_device) {
-      CUDA_TRY(cudaMemcpyAsync(counters_out, dst, T * K_NCTR * 4, cudaMemcpyDeviceToHost, st));
-      cudaFreeAsync(dst, st);
-    }
+    if (!on_device)
+      CUDA_TRY(cudaMemcpyAsync(counters_out, dst, ctr_bytes, cudaMemcpyDeviceToHost, st));
   }
   if (hist_out) {
     unsigned long long* dst = nullptr;

@@ -2034,7 +2034,13 @@ __device__ __forceinline__ void run_item(const StepArgs& args, const uint32_t* t
 // bucketed order.  Small pools launch CTAs for the first kMainItems(T) items
 // only (the heavy share of a step is about half); the rest, if any, run on
 // the overflow kernel below.
-__global__ void __launch_bounds__(kWarpsPerCta * kCrew * 32, 32 / (kWarpsPerCta * kCrew))
+#ifndef RKC_BIG_MIN_CTAS
+#define RKC_BIG_MIN_CTAS (32 / (kCrew))
+#endif
+// resident CTAs per SM the register budget is sized for (small pools: 32 one-warp
+// CTAs = 64 registers; big pools: crews of kCrew warps)
+constexpr int kMinCtas = kBig ? RKC_BIG_MIN_CTAS : 32 / kWarpsPerCta;
+__global__ void __launch_bounds__(kWarpsPerCta * kCrew * 32, kMinCtas)
 rkc_step_kernel(const __grid_constant__ StepArgs args) {
   pdl_wait();
   const uint32_t* tk;

@@ -92,7 +92,8 @@ def test_slot_stress_parity_all_slots(N):
     k = ops["kind"]
     assert ops["a"][k == gen.SUBMIT].max() == 31
     assert ops["a"][(k == gen.ADMIT) | (k == gen.ADVANCE)].max() == 31
-    assert max(ops["a"][k == gen.INSERT].max(), ops["b"][k == gen.ADMIT].max()) == 127
+    assert max(ops["a"][k == gen.INSERT].max(), ops["b"][k == gen.ADMIT].max(),
+               ops["b"][k == gen.SUBMIT].max()) >= 120
     if N > 1024:     # big pools: usable sizes well below N keep the pressure on
         cfgs["U"] = np.random.default_rng(N).integers(N // 6, N // 2, size=len(cfgs))
     g = run_gpu(cfgs, ops, N=N, C=32, Q=32, O=128)

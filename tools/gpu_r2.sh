@@ -9,6 +9,6 @@ timeout 1500 python -m pytest tests -m gpu -x -q --durations=20 > $OUT/gpu_tests
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
 if [ "${N2:-1}" = "1" ]; then
-  timeout 900 python bench.py --gpus 2 --steps 3 --no-cpu-baseline > $OUT/bench_n2.json 2> $OUT/bench_n2.err; echo "bench n2 rc=$?" >> $OUT/bench_n2.err
+  RKC_BENCH_WATCHDOG=500 timeout 600 python bench.py --gpus 2 --steps 3 --no-cpu-baseline > $OUT/bench_n2.json 2> $OUT/bench_n2.err; echo "bench n2 rc=$?" >> $OUT/bench_n2.err
 fi
 ls -la $OUT

@@ -18,19 +18,20 @@ def main():
     ap.add_argument("--steps", type=int, default=256)
     ap.add_argument("--blocks", type=int, default=1024)
     ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--objects", type=int, default=64)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--nop", action="store_true", help="all-NOP op stream (launch floor)")
     ap.add_argument("--tag", default="")
     a = ap.parse_args()
     import torch
     from paper_2605_24259_b200 import gen, rkc
-    cfgs, ops = gen.random_traces(a.config, 0, 0, a.traces, a.steps, a.blocks)
+    cfgs, ops = gen.random_traces(a.config, 0, 0, a.traces, a.steps, a.blocks, 16, 16, a.objects)
     if a.nop:
         ops[:] = np.zeros((), dtype=ops.dtype)
     non_nop = int((ops["kind"] != 0).sum())
     d = torch.from_numpy(ops.view(np.uint8).reshape(-1)).cuda()
     ept = max(64, 2 * a.steps + 64)
-    pool = rkc.Pool(cfgs, a.blocks, 16, 16, 64, events_per_trace=ept)
+    pool = rkc.Pool(cfgs, a.blocks, 16, 16, a.objects, events_per_trace=ept)
     ts = []
     for r in range(a.reps + 1):
         pool.rkc_pool_reset()
