@@ -1764,19 +1764,30 @@ __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_c
   __shared__ uint32_t s_cnt[8], s_base[8];
   if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
   __syncthreads();
+  // level 1 (the op and the trace's hot header) is software-pipelined: the
+  // loads of the next iteration's trace are in flight while this one runs
+  uint4 nop = make_uint4(0, 0, 0, 0), nh0 = nop, nh1 = nop, nh2 = nop;
+  auto fetch = [&](uint32_t b) {
+    const uint32_t tn = b + threadIdx.x;
+    if (tn < p.num_traces) {
+      nop = __ldcs(args.ops + tn);
+      const uint4* h4 = reinterpret_cast<const uint4*>(p.hdr + (size_t)tn * H_NWORDS);
+      nh0 = __ldcg(h4);      // U, policy, accept, seq
+      nh1 = __ldcg(h4 + 1);  // free, alive, P, mask
+      nh2 = __ldcg(h4 + 2);  // next expiry, event count
+    }
+  };
+  fetch(blockIdx.x * blockDim.x);
   for (uint32_t base = blockIdx.x * blockDim.x; base < p.num_traces; base += stride) {
     const uint32_t t = base + threadIdx.x;
     const bool valid = t < p.num_traces;
     bool heavy = false, fa = false;
     uint32_t kind = 0, fa_need = 0, fa_live = 0, fa_owner = 0;
     uint4 opw = make_uint4(0, 0, 0, 0), hv0 = opw, hv1 = opw, hv2 = opw;
+    if (valid) { opw = nop; hv0 = nh0; hv1 = nh1; hv2 = nh2; }
+    fetch(base + stride);
     if (valid) {
-      // level 1: the op and the trace's hot header (independent of the op)
-      opw = __ldcs(args.ops + t);
       const uint32_t* h = p.hdr + (size_t)t * H_NWORDS;
-      hv0 = __ldcg(reinterpret_cast<const uint4*>(h));      // U, policy, accept, seq
-      hv1 = __ldcg(reinterpret_cast<const uint4*>(h) + 1);  // free, alive, P, mask
-      hv2 = __ldcg(reinterpret_cast<const uint4*>(h) + 2);  // next expiry, event count
       const uint32_t nexp = hv2.x;
       kind = opw.x & 0xFFu;
       const uint32_t a = (opw.x >> 8) & 0xFFu;
