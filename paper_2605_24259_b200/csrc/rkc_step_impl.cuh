@@ -1753,6 +1753,13 @@ __device__ __forceinline__ uint32_t bucket_of(uint32_t kind) {
 #define RKC_LIGHT_THREADS 128
 #endif
 constexpr uint32_t kLightThreads = RKC_LIGHT_THREADS;
+// heavy-trace ticket: op (4 words), hot header words 0..11 (word 10 <- the trace
+// id), and with RKC_TICKET_RQ the request record of an ADVANCE (8 words, read
+// by the light pass anyway) so the step kernel skips that dependent load
+#ifndef RKC_TICKET_RQ
+#define RKC_TICKET_RQ 0
+#endif
+constexpr uint32_t kTicketWords = RKC_TICKET_RQ ? 24u : 16u;
 __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_constant__ StepArgs args) {
   const PoolDev& p = args.p;
   const uint32_t step = args.step;
@@ -1764,30 +1771,20 @@ __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_c
   __shared__ uint32_t s_cnt[8], s_base[8];
   if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
   __syncthreads();
-  // level 1 (the op and the trace's hot header) is software-pipelined: the
-  // loads of the next iteration's trace are in flight while this one runs
-  uint4 nop = make_uint4(0, 0, 0, 0), nh0 = nop, nh1 = nop, nh2 = nop;
-  auto fetch = [&](uint32_t b) {
-    const uint32_t tn = b + threadIdx.x;
-    if (tn < p.num_traces) {
-      nop = __ldcs(args.ops + tn);
-      const uint4* h4 = reinterpret_cast<const uint4*>(p.hdr + (size_t)tn * H_NWORDS);
-      nh0 = __ldcg(h4);      // U, policy, accept, seq
-      nh1 = __ldcg(h4 + 1);  // free, alive, P, mask
-      nh2 = __ldcg(h4 + 2);  // next expiry, event count
-    }
-  };
-  fetch(blockIdx.x * blockDim.x);
   for (uint32_t base = blockIdx.x * blockDim.x; base < p.num_traces; base += stride) {
     const uint32_t t = base + threadIdx.x;
     const bool valid = t < p.num_traces;
     bool heavy = false, fa = false;
     uint32_t kind = 0, fa_need = 0, fa_live = 0, fa_owner = 0;
     uint4 opw = make_uint4(0, 0, 0, 0), hv0 = opw, hv1 = opw, hv2 = opw;
-    if (valid) { opw = nop; hv0 = nh0; hv1 = nh1; hv2 = nh2; }
-    fetch(base + stride);
+    uint4 rqa = opw, rqb = opw;  // an ADVANCE's request record (ticket words 16..23)
     if (valid) {
+      // level 1: the op and the trace's hot header (independent of the op)
+      opw = __ldcs(args.ops + t);
       const uint32_t* h = p.hdr + (size_t)t * H_NWORDS;
+      hv0 = __ldcg(reinterpret_cast<const uint4*>(h));      // U, policy, accept, seq
+      hv1 = __ldcg(reinterpret_cast<const uint4*>(h) + 1);  // free, alive, P, mask
+      hv2 = __ldcg(reinterpret_cast<const uint4*>(h) + 2);  // next expiry, event count
       const uint32_t nexp = hv2.x;
       kind = opw.x & 0xFFu;
       const uint32_t a = (opw.x >> 8) & 0xFFu;
@@ -1799,6 +1796,8 @@ __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_c
         uint32_t* rq = p.req + ((size_t)t * p.Q + a) * 8;
         const uint4 r0 = __ldcg(reinterpret_cast<const uint4*>(rq));
         const uint4 r1 = __ldcg(reinterpret_cast<const uint4*>(rq + 4));
+        rqa = r0;
+        rqb = r1;
         const bool small = p.NS <= 1024;  // one bitmap word per lane
         const uint32_t status = r0.x & 0xFFu, prompt = r0.y, chunk = r0.z, decode = r0.w;
         const uint32_t done = r1.x, live = r1.y, held = r1.y + r1.z;  // own + shared hit blocks
@@ -1905,13 +1904,14 @@ __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_c
       s_cnt[threadIdx.x] = 0;
     }
     __syncthreads();
-    if (heavy) {  // the 64-B ticket: op, header words 0..11 (word 10 <- the trace id)
+    if (heavy) {  // the ticket: op, header words 0..11 (word 10 <- the trace id)[, request]
       uint4* tk = reinterpret_cast<uint4*>(p.perm) +
-                  4 * ((size_t)bk * p.num_traces + s_base[bk] + off + __popc(grp & lanemask_lt()));
+                  (kTicketWords / 4) * ((size_t)bk * p.num_traces + s_base[bk] + off + __popc(grp & lanemask_lt()));
       tk[0] = opw;
       tk[1] = hv0;
       tk[2] = hv1;
       tk[3] = make_uint4(hv2.x, hv2.y, t, 0u);
+      if (RKC_TICKET_RQ && kind == OP_ADVANCE) { tk[4] = rqa; tk[5] = rqb; }
     }
   }
 }
@@ -1931,7 +1931,7 @@ __device__ __forceinline__ bool item_trace(const StepArgs& args, uint32_t i, con
     acc += c;
   }
   if (bk == 8) return false;
-  tk = args.p.perm + ((size_t)bk * args.p.num_traces + off) * 16;
+  tk = args.p.perm + ((size_t)bk * args.p.num_traces + off) * kTicketWords;
   return true;
 }
 
@@ -1948,7 +1948,7 @@ __device__ __forceinline__ void run_item(const StepArgs& args, const uint32_t* t
   // the ticket (written by the light pass, read through L1): lane l < 16 holds
   // word l -- the op in words 0..3, header words 0..11 in 4..15, the trace id
   // in place of (unused) header word 10
-  const uint32_t tw = lane < 16 ? __ldg(tk + lane) : 0u;
+  const uint32_t tw = lane < kTicketWords ? __ldg(tk + lane) : 0u;
   const uint4 opw = make_uint4(__shfl_sync(kFull, tw, 0), __shfl_sync(kFull, tw, 1),
                                __shfl_sync(kFull, tw, 2), __shfl_sync(kFull, tw, 3));
   const uint32_t t = __shfl_sync(kFull, tw, 14);
@@ -1964,7 +1964,12 @@ __device__ __forceinline__ void run_item(const StepArgs& args, const uint32_t* t
   const bool want_ob = kind == OP_SUBMIT || kind == OP_INSERT || kind == OP_COMPLETE ||
                        kind == OP_TOUCH || kind == OP_HIT_ADMIT;
   uint32_t rqv = 0;
-  if (rq_op && lane < 8) rqv = __ldcg(p.req + ((size_t)t * p.Q + a) * 8 + lane);
+  if (RKC_TICKET_RQ && kind == OP_ADVANCE && a < p.Q) {
+    rqv = __shfl_sync(kFull, tw, (lane + 16) & 31u);  // from the ticket (light pass read it)
+    if (lane >= 8) rqv = 0;
+  } else if (rq_op && lane < 8) {
+    rqv = __ldcg(p.req + ((size_t)t * p.Q + a) * 8 + lane);
+  }
   uint4 c0 = make_uint4(0, 0, 0, 0), c1 = make_uint4(0, 0, 0, 0);
   if (want_cl && lane < p.C) {
     const uint4* cp = reinterpret_cast<const uint4*>(p.clm + ((size_t)t * p.C + lane) * 8);
@@ -2061,7 +2066,7 @@ rkc_step_kernel(const __grid_constant__ StepArgs args) {
 
 #if !RKC_BIG
 #ifndef RKC_MAIN_SIXTEENTHS
-#define RKC_MAIN_SIXTEENTHS 10
+#define RKC_MAIN_SIXTEENTHS 9
 #endif
 __host__ __device__ constexpr uint32_t kMainItems(uint32_t T) {  // RKC_MAIN_SIXTEENTHS/16 of T
   return (uint32_t)(((uint64_t)T * RKC_MAIN_SIXTEENTHS + 15) / 16);
@@ -2069,8 +2074,16 @@ __host__ __device__ constexpr uint32_t kMainItems(uint32_t T) {  // RKC_MAIN_SIX
 // items [kMainItems(T), heavy count), if any: a grid of 1/16 of the remaining
 // slots (at least 592 CTAs) loops over them, at most 16 items per warp -- a
 // step with more heavy traces than the main grid slows down gradually
+#ifndef RKC_OVF_MAX_CTAS
+#define RKC_OVF_MAX_CTAS (148u * 16u)
+#endif
 __host__ __device__ constexpr uint32_t kOverflowCtas(uint32_t T) {
-  return (T - kMainItems(T)) / 16 > 592 ? (T - kMainItems(T)) / 16 : 592;
+  // capped: every overflow CTA is dispatched every step even when no item
+  // overflows (~0.5 ns each), and c5 would otherwise launch 27k of them
+  return (T - kMainItems(T)) / 16 > 592
+             ? ((T - kMainItems(T)) / 16 < (uint32_t)(RKC_OVF_MAX_CTAS) ? (T - kMainItems(T)) / 16
+                                                                        : (uint32_t)(RKC_OVF_MAX_CTAS))
+             : 592;
 }
 __global__ void __launch_bounds__(32) rkc_step_overflow_kernel(const __grid_constant__ StepArgs args) {
   pdl_wait();
@@ -2103,7 +2116,12 @@ static cudaError_t launch_pdl(Kernel kernel, uint32_t grid, uint32_t block, cuda
 cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, cudaStream_t st) {
   StepArgs args{p, reinterpret_cast<const uint4*>(ops_step), step};
   const uint32_t lct = (p.num_traces + kLightThreads - 1) / kLightThreads;
-  const uint32_t cgrid = lct < 148 * 2048 / kLightThreads ? lct : 148 * 2048 / kLightThreads;
+// one light thread per trace (round 2: the former cap of 16 CTAs per SM, i.e. 3.3 traces per
+// thread at c5, measured 1 % slower per lockstep step: profiles/r02/experiments.md)
+#ifndef RKC_LIGHT_MAX_CTAS
+#define RKC_LIGHT_MAX_CTAS 0x7FFFFFFF
+#endif
+  const uint32_t cgrid = lct < (uint32_t)(RKC_LIGHT_MAX_CTAS) ? lct : (uint32_t)(RKC_LIGHT_MAX_CTAS);
   cudaError_t e = launch_pdl(rkc_light_kernel, cgrid, kLightThreads, st, args);
 #if RKC_BIG
   if (e == cudaSuccess)
