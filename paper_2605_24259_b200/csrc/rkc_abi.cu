@@ -455,7 +455,7 @@ rkc_status rkc_pool_create(const rkc_pool_config* config, const rkc_trace_config
   ALLOC(d.obj, T * d.O * 8);
   ALLOC(d.ctr, T * K_NCTR * 4);
   ALLOC(d.ev, T * (size_t)d.EPT * 32);
-  ALLOC(d.perm, T * 8 * 96);   // tickets: up to 24 words (rkc_step_impl.cuh kTicketWords)
+  ALLOC(d.perm, T * 8 * 64);   // 64-B tickets (rkc_step_impl.cuh kTicketWords)
   ALLOC(d.bcnt, 16 * 4);
   ALLOC(p->tcfg, T * 12);
   ALLOC(p->staged, T * 16);

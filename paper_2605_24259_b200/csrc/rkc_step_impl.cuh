@@ -1753,13 +1753,8 @@ __device__ __forceinline__ uint32_t bucket_of(uint32_t kind) {
 #define RKC_LIGHT_THREADS 128
 #endif
 constexpr uint32_t kLightThreads = RKC_LIGHT_THREADS;
-// heavy-trace ticket: op (4 words), hot header words 0..11 (word 10 <- the trace
-// id), and with RKC_TICKET_RQ the request record of an ADVANCE (8 words, read
-// by the light pass anyway) so the step kernel skips that dependent load
-#ifndef RKC_TICKET_RQ
-#define RKC_TICKET_RQ 0
-#endif
-constexpr uint32_t kTicketWords = RKC_TICKET_RQ ? 24u : 16u;
+// heavy-trace ticket: op (4 words), hot header words 0..11 (word 10 <- the trace id)
+constexpr uint32_t kTicketWords = 16u;
 __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_constant__ StepArgs args) {
   const PoolDev& p = args.p;
   const uint32_t step = args.step;
@@ -1777,7 +1772,6 @@ __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_c
     bool heavy = false, fa = false;
     uint32_t kind = 0, fa_need = 0, fa_live = 0, fa_owner = 0;
     uint4 opw = make_uint4(0, 0, 0, 0), hv0 = opw, hv1 = opw, hv2 = opw;
-    uint4 rqa = opw, rqb = opw;  // an ADVANCE's request record (ticket words 16..23)
     if (valid) {
       // level 1: the op and the trace's hot header (independent of the op)
       opw = __ldcs(args.ops + t);
@@ -1796,8 +1790,6 @@ __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_c
         uint32_t* rq = p.req + ((size_t)t * p.Q + a) * 8;
         const uint4 r0 = __ldcg(reinterpret_cast<const uint4*>(rq));
         const uint4 r1 = __ldcg(reinterpret_cast<const uint4*>(rq + 4));
-        rqa = r0;
-        rqb = r1;
         const bool small = p.NS <= 1024;  // one bitmap word per lane
         const uint32_t status = r0.x & 0xFFu, prompt = r0.y, chunk = r0.z, decode = r0.w;
         const uint32_t done = r1.x, live = r1.y, held = r1.y + r1.z;  // own + shared hit blocks
@@ -1911,7 +1903,6 @@ __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_c
       tk[1] = hv0;
       tk[2] = hv1;
       tk[3] = make_uint4(hv2.x, hv2.y, t, 0u);
-      if (RKC_TICKET_RQ && kind == OP_ADVANCE) { tk[4] = rqa; tk[5] = rqb; }
     }
   }
 }
@@ -1964,12 +1955,7 @@ __device__ __forceinline__ void run_item(const StepArgs& args, const uint32_t* t
   const bool want_ob = kind == OP_SUBMIT || kind == OP_INSERT || kind == OP_COMPLETE ||
                        kind == OP_TOUCH || kind == OP_HIT_ADMIT;
   uint32_t rqv = 0;
-  if (RKC_TICKET_RQ && kind == OP_ADVANCE && a < p.Q) {
-    rqv = __shfl_sync(kFull, tw, (lane + 16) & 31u);  // from the ticket (light pass read it)
-    if (lane >= 8) rqv = 0;
-  } else if (rq_op && lane < 8) {
-    rqv = __ldcg(p.req + ((size_t)t * p.Q + a) * 8 + lane);
-  }
+  if (rq_op && lane < 8) rqv = __ldcg(p.req + ((size_t)t * p.Q + a) * 8 + lane);
   uint4 c0 = make_uint4(0, 0, 0, 0), c1 = make_uint4(0, 0, 0, 0);
   if (want_cl && lane < p.C) {
     const uint4* cp = reinterpret_cast<const uint4*>(p.clm + ((size_t)t * p.C + lane) * 8);

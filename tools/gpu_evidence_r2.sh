@@ -1,0 +1,19 @@
+#!/bin/bash
+# Round-2 evidence on the committed build: GPU tests, smoke, benches (c5 default, c3, c6, c4),
+# the 10^6-trace single-pool parity run, compute-sanitizer on small shapes.
+set -x
+OUT=gpurun_out; mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks_event_reasons.active --format=csv > $OUT/smi.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -q --durations=25 > $OUT/gpu_tests.log 2>&1; echo "pytest rc=$?" >> $OUT/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
+timeout 900 python bench.py > $OUT/bench_c5.json 2> $OUT/bench_c5.err; echo "rc=$?" >> $OUT/bench_c5.err
+timeout 900 python bench.py --config c3 > $OUT/bench_c3.json 2> $OUT/bench_c3.err; echo "rc=$?" >> $OUT/bench_c3.err
+timeout 900 python bench.py --config c6 > $OUT/bench_c6.json 2> $OUT/bench_c6.err; echo "rc=$?" >> $OUT/bench_c6.err
+timeout 1500 python bench.py --config c4 > $OUT/bench_c4.json 2> $OUT/bench_c4.err; echo "rc=$?" >> $OUT/bench_c4.err
+timeout 600 python bench.py --impl reference > $OUT/bench_reference.json 2> $OUT/bench_reference.err; echo "rc=$?" >> $OUT/bench_reference.err
+timeout 2400 python tests/run_parity_1m.py --single-pool --chunk 50000 > $OUT/parity_1m_single_pool.log 2>&1; echo "rc=$?" >> $OUT/parity_1m_single_pool.log
+CS=/usr/local/cuda/bin/compute-sanitizer
+timeout 1500 $CS --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_parity.py tests/test_gpu_boundary.py -x -q -k "paper_litmus or pool_sizes or slot_stress_parity_all_slots or c4_subset or reserve or drain or staging or malformed or leading or spec" > $OUT/sanitize_memcheck.log 2>&1; echo "rc=$?" >> $OUT/sanitize_memcheck.log
+timeout 900 $CS --tool racecheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/sanitize_racecheck.log 2>&1; echo "rc=$?" >> $OUT/sanitize_racecheck.log
+timeout 900 $CS --tool synccheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/sanitize_synccheck.log 2>&1; echo "rc=$?" >> $OUT/sanitize_synccheck.log
+ls -la $OUT
