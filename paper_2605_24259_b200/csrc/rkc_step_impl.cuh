@@ -351,34 +351,6 @@ __device__ __forceinline__ void crew_bar() {
 }
 __device__ __forceinline__ uint32_t crew_j0(uint32_t w) { return S.nv * w / kCrew; }
 
-// Stream block vectors [j0, j1) of `base` with kCrewAhead loads in flight: the
-// load of vector j + kCrewAhead is issued before vector j is processed, so a
-// pass that also stores (apply, release, complete, touch, reclass) keeps its
-// loads overlapped -- the compiler cannot hoist a load above a store it cannot
-// prove disjoint, and f(j, v) only writes words of vector j.  f returns false
-// to stop early.
-#ifndef RKC_CREW_AHEAD
-#define RKC_CREW_AHEAD 0
-#endif
-constexpr int kCrewAhead = RKC_CREW_AHEAD;
-template <class F>
-__device__ __forceinline__ void crew_stream(const uint4* base, uint32_t j0, uint32_t j1, F&& f) {
-  const uint32_t lane = lane_id();
-  uint4 buf[kCrewAhead > 0 ? kCrewAhead : 1];
-#pragma unroll
-  for (int q = 0; q < kCrewAhead; ++q)
-    buf[q] = j0 + q < j1 ? __ldcg(base + (j0 + q) * 32 + lane) : make_uint4(0, 0, 0, 0);
-  for (uint32_t j = j0; j < j1; j += kCrewAhead) {
-#pragma unroll
-    for (int q = 0; q < kCrewAhead; ++q) {
-      const uint4 v = buf[q];
-      const uint32_t jn = j + kCrewAhead + q;
-      buf[q] = jn < j1 ? __ldcg(base + jn * 32 + lane) : make_uint4(0, 0, 0, 0);
-      if (j + q >= j1 || !f(j + q, v)) return;
-    }
-  }
-}
-
 // one job's slice for warp w (lane = lane_id()); arguments in S.job[1..7]
 __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
   const uint32_t lane = lane_id();
@@ -434,11 +406,11 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
       uint32_t rank = 0;
       for (uint32_t v = 0; v < w; ++v) rank += S.red[v][0];
       const uint32_t end = rank + S.red[w][0];
-      auto apply_vec = [&](uint32_t j, const uint4 v) -> bool {
-        if (rank >= end) return false;
+      for (uint32_t j = j0; j < j1 && rank < end; ++j) {
+        const uint4 v = __ldcg(key4 + j * 32 + lane);
         const uint32_t tb = (v.x <= T ? 1u : 0u) | (v.y <= T ? 2u : 0u) | (v.z <= T ? 4u : 0u) |
                             (v.w <= T ? 8u : 0u);
-        if (!__any_sync(kFull, tb != 0)) return true;
+        if (!__any_sync(kFull, tb != 0)) continue;
         const uint32_t cnt = __popc(tb);
         const uint32_t Sc = warp_incl_scan(cnt, lane);
         uint32_t r = rank + Sc - cnt;
@@ -468,13 +440,6 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
           }
         }
         rank += __shfl_sync(kFull, Sc, 31);
-        return true;
-      };
-      if (kCrewAhead > 0) {
-        crew_stream(key4, j0, j1, apply_vec);
-      } else {
-        for (uint32_t j = j0; j < j1; ++j)
-          if (!apply_vec(j, __ldcg(key4 + j * 32 + lane))) break;
       }
       for (uint32_t wi = j0 * 4 + lane; wi < j1 * 4; wi += 32) S.fbm[wi] = 0;  // every free block was taken
       r1 = __reduce_add_sync(kFull, r1);
@@ -484,7 +449,9 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
     }
     case JOB_RELEASE: {  // request S.job[1]'s active blocks -> FREE
       const uint32_t rq = S.job[1];
-      auto release_vec = [&](uint32_t j, const uint4 mv) -> bool {
+#pragma unroll(kCrewUnroll)
+      for (uint32_t j = j0; j < j1; ++j) {
+        const uint4 mv = __ldcg(meta4 + j * 32 + lane);
         uint32_t nib = 0;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -502,13 +469,6 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
           fbm_set(j, nib);
           r0 += __popc(nib);
         }
-        return true;
-      };
-      if (kCrewAhead > 0) {
-        crew_stream(meta4, j0, j1, release_vec);
-      } else {
-#pragma unroll(kCrewUnroll)
-        for (uint32_t j = j0; j < j1; ++j) release_vec(j, __ldcg(meta4 + j * 32 + lane));
       }
       r0 = __reduce_add_sync(kFull, r0);
       break;
@@ -516,7 +476,9 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
     case JOB_COMPLETE: {  // request a's blocks: full ones -> CACHED(o) tail-first stamps, rest -> FREE
       const uint32_t a = S.job[1], full = S.job[2], o = S.job[3], lim3 = S.job[4], lim2 = S.job[5];
       const uint32_t seq_base = S.job[6];
-      auto complete_vec = [&](uint32_t j, const uint4 mv) -> bool {
+#pragma unroll(kCrewUnroll)
+      for (uint32_t j = j0; j < j1; ++j) {
+        const uint4 mv = __ldcg(meta4 + j * 32 + lane);
         uint32_t nib = 0;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -536,20 +498,15 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
         }
         fbm_set(j, nib);
         r0 += __popc(nib);
-        return true;
-      };
-      if (kCrewAhead > 0) {
-        crew_stream(meta4, j0, j1, complete_vec);
-      } else {
-#pragma unroll(kCrewUnroll)
-        for (uint32_t j = j0; j < j1; ++j) complete_vec(j, __ldcg(meta4 + j * 32 + lane));
       }
       r0 = __reduce_add_sync(kFull, r0);
       break;
     }
     case JOB_TOUCH: {  // restamp object S.job[1]'s leading prefix [0, L) tail-first
       const uint32_t ob = S.job[1], L = S.job[2], seq_base = S.job[3];
-      auto touch_vec = [&](uint32_t j, const uint4 mv) -> bool {
+#pragma unroll(kCrewUnroll)
+      for (uint32_t j = j0; j < j1; ++j) {
+        const uint4 mv = __ldcg(meta4 + j * 32 + lane);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const uint32_t m = el(mv, e);
@@ -558,25 +515,20 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
             key[bb] = (__ldcg(key + bb) & ~kSeqMask) | (seq_base + (L - 1 - meta_pos(m)));
           }
         }
-        return true;
-      };
-      if (kCrewAhead > 0) {
-        crew_stream(meta4, j0, j1, touch_vec);
-      } else {
-#pragma unroll(kCrewUnroll)
-        for (uint32_t j = j0; j < j1; ++j) touch_vec(j, __ldcg(meta4 + j * 32 + lane));
       }
       break;
     }
     case JOB_RECLASS: {  // class bits of the marked objects' cached blocks (S.lim3 / S.lim2 / S.cnt3)
-      auto reclass_vec = [&](uint32_t j, const uint4 mv) -> bool {
+#pragma unroll(kCrewUnroll)
+      for (uint32_t j = j0; j < j1; ++j) {
+        const uint4 mv = __ldcg(meta4 + j * 32 + lane);
         bool any = false;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const uint32_t m = el(mv, e);
           any |= meta_res(m) == kResCached && in_reclass(meta_owner(m));
         }
-        if (!any) return true;
+        if (!any) continue;
         const uint4 kv = __ldcg(key4 + j * 32 + lane);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -592,13 +544,6 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
           if (k1 != k0) key[block_of(j, e)] = k1;
           if (cls == 3 && !pin) atomicAdd(&S.cnt3[o], 1u);
         }
-        return true;
-      };
-      if (kCrewAhead > 0) {
-        crew_stream(meta4, j0, j1, reclass_vec);
-      } else {
-#pragma unroll(kCrewUnroll)
-        for (uint32_t j = j0; j < j1; ++j) reclass_vec(j, __ldcg(meta4 + j * 32 + lane));
       }
       break;
     }
@@ -2096,7 +2041,10 @@ __device__ __forceinline__ void run_item(const StepArgs& args, const uint32_t* t
 #endif
 // resident CTAs per SM the register budget is sized for (small pools: 32 one-warp
 // CTAs = 64 registers; big pools: crews of kCrew warps)
-constexpr int kMinCtas = kBig ? RKC_BIG_MIN_CTAS : 32 / kWarpsPerCta;
+#ifndef RKC_SMALL_MIN_CTAS
+#define RKC_SMALL_MIN_CTAS (32 / kWarpsPerCta)
+#endif
+constexpr int kMinCtas = kBig ? RKC_BIG_MIN_CTAS : RKC_SMALL_MIN_CTAS;
 __global__ void __launch_bounds__(kWarpsPerCta * kCrew * 32, kMinCtas)
 rkc_step_kernel(const __grid_constant__ StepArgs args) {
   pdl_wait();
