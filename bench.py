@@ -50,6 +50,11 @@ WORKLOADS = {
                desc="c6: c3 + prefix hits (NEXT f3): 100k random traces per GPU, 1024-block pools, "
                     "T=256 lockstep steps, half of the admissions share a known object's surviving prefix",
                l2="inputs larger than L2: pool state 0.83 GB + ops 0.41 GB per GPU, no flush"),
+    # c8 (NEXT f4): the c3 recipe with admission under the resident reserve on 40 % of the traces
+    "c8": dict(recipe=8, traces=100_000, nblk=1024, steps=256, C=16, Q=16, O=64, ept=512,
+               desc="c8: c3 + resident-reserve admission (NEXT f4): 100k random traces per GPU, "
+                    "1024-block pools, T=256 lockstep steps, admit_check PEAK/NONE/RESERVE .4/.2/.4",
+               l2="inputs larger than L2: pool state 0.83 GB + ops 0.41 GB per GPU, no flush"),
     # c5 (configs[4]): 10^6 c3 traces in total, sharded over the ranks (strong scaling)
     "c5": dict(recipe=3, traces=1_000_000, nblk=1024, steps=256, C=16, Q=16, O=64, ept=512, strong=True,
                desc="c5: 10^6 random c3 traces sharded over the GPUs (1024-block pools, T=256 lockstep "

@@ -36,6 +36,9 @@ def main():
     ap.add_argument("--blocks", type=int, default=1024)
     ap.add_argument("--config", type=int, default=3, help="generator recipe (3 = c3/c5, 6 = c6 hits)")
     ap.add_argument("--single-pool", action="store_true")
+    ap.add_argument("--slots", type=int, nargs=3, default=(16, 16, 64), metavar=("C", "Q", "O"))
+    ap.add_argument("--u-range", type=int, nargs=2, default=None, metavar=("LO", "HI"),
+                    help="draw each trace's usable blocks from [LO, HI] (seeded) instead of N")
     a = ap.parse_args()
     import torch
     from paper_2605_24259_b200 import gen
@@ -66,9 +69,13 @@ def single_pool(a, threads, t0):
     import torch
     from paper_2605_24259_b200 import gen, rkc
     from parity_util import VIEW_KEYS, first_event_mismatch, run_ref
+    C, Q, O = a.slots
     cfgs, ops = gen.random_traces(a.config, seed=0, trace_begin=0, n_traces=a.traces, T=a.steps,
-                                  N=a.blocks)
-    pool = rkc.Pool(cfgs, a.blocks, events_per_trace=512)
+                                  N=a.blocks, C=C, Q=Q, O=O)
+    if a.u_range:
+        cfgs["U"] = np.random.default_rng(0).integers(a.u_range[0], a.u_range[1] + 1, size=a.traces)
+    ept = max(512, 4 * a.steps + 64)
+    pool = rkc.Pool(cfgs, a.blocks, C, Q, O, events_per_trace=ept)
     pool.rkc_step_batch(torch.from_numpy(ops.view(np.uint8).reshape(-1)).cuda(), a.steps)
     torch.cuda.synchronize()
     counters, events, _ = pool.read_all()
@@ -79,7 +86,7 @@ def single_pool(a, threads, t0):
     for begin in range(0, a.traces, a.chunk):
         n = min(a.chunk, a.traces - begin)
         sub = np.ascontiguousarray(ops[:, begin:begin + n])
-        o = run_ref(cfgs[begin:begin + n], sub, N=a.blocks, nthreads=threads)
+        o = run_ref(cfgs[begin:begin + n], sub, N=a.blocks, C=C, Q=Q, O=O, nthreads=threads)
         oe = o["events"]
         oe["trace"] += begin
         ge = events[idx[begin]:idx[begin + n]]
@@ -95,6 +102,7 @@ def single_pool(a, threads, t0):
         print(f"traces [{begin:7d}, {begin + n:7d}) bit-exact in the single pool "
               f"({time.time() - t0:.0f} s)", flush=True)
     print(json.dumps({"config": a.config, "traces": a.traces, "steps": a.steps, "pool_blocks": a.blocks,
+                      "slots": [C, Q, O], "u_range": a.u_range,
                       "layout": "one pool of all traces (the bench launch configuration)",
                       "non_nop_ops": n_ops, "events": len(events), "result": "bit-exact",
                       "host_threads": threads, "seconds": round(time.time() - t0, 1)}))
