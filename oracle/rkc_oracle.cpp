@@ -20,10 +20,14 @@
  *
  * Parity pins: see DESIGN.md "Oracle pins" -- every function below is pinned
  * by tests/test_oracle_*.py against paper numbers, closed forms, brute force
- * or invariants, except the orderings that the paper leaves open (G1 LRU
- * tail-first stamps, G6 soft bucket, G10 auto-demotion order, G18 event
- * order, G24 block-to-position order): those are "parity unpinned" by the
- * paper and fixed only by the ledger.
+ * or invariants.  The orderings the paper leaves open are the ledger's
+ * readings, each pinned by a closed form or a property the paper states:
+ * G1 tail-first stamps by P:615-616 "survived positions form leading ranges"
+ * (invariant I11, asserted after every op in check mode) and the L-ORD
+ * closed form; G6 soft bucket by the L-SOFT closed form and the exhaustive
+ * victim search; G10 auto-demotion order and G18 event order by closed forms
+ * (tests/test_oracle_readings.py); G24 block-to-position order by the
+ * exhaustive victim search.  tools/oracle_mutants.py flips each of them.
  */
 #include <algorithm>
 #include <atomic>
@@ -129,7 +133,8 @@ struct Trace {
   std::vector<EventRec> events;
   uint32_t t = 0;          /* current step index */
   uint32_t ev_seq = 0;     /* emission index within (trace, step), G18 */
-  bool check = false;      /* assert invariants I1-I9 after every op */
+  bool check = false;      /* assert invariants I1-I11 after every op */
+  bool injected = false;   /* state imported from views (I11 holds only for states it built) */
   int violation = 0;       /* first invariant violated (1..9), 0 = none */
   std::vector<uint32_t> lead_prev;  /* I8 bookkeeping (debug mode only) */
 
@@ -739,6 +744,18 @@ struct Trace {
     /* I4: contract traces never harm an obligated claim (north star) */
     for (const EventRec& e : events)
       if (e.step == t && e.type == E_CLAIM_HARMED && e.reason == 1 && cfg.lowering == LOW_CONTRACT) fail(4);
+    /* I11: "survived positions form leading ranges" (the paper's
+     * ledger check on its vLLM traces): every live object's cached
+     * positions are exactly [0, leading(o)).  This is what the tail-first
+     * stamp order (G1) guarantees -- eviction eats each chain from its tail;
+     * a head-first order would strand the tail.  (Injected states, e.g. L6's
+     * position-0 hole, are exempt: they were not built by the runtime.) */
+    if (!injected) {
+      std::vector<uint32_t> cached(obj.size(), 0);
+      for (const Block& b : blk) if (b.res == B_CACHED) cached[b.owner]++;
+      for (uint32_t o = 0; o < obj.size(); ++o)
+        if (obj[o].live && cached[o] != leading(o)) fail(11);
+    }
     /* I9: running requests hold exactly ceil(done/16) blocks */
     for (const Request& r : req)
       if (r.status == R_RUNNING && r.hit + r.live != (r.done + BLOCK_TOKENS - 1) / BLOCK_TOKENS) fail(9);
@@ -880,6 +897,7 @@ void oracle_trace_import(void* h, uint32_t trace, uint32_t seq_ctr, uint32_t ste
   Batch* b = (Batch*)h;
   Trace& tr = b->traces[trace];
   tr.seq_ctr = seq_ctr; tr.t = step;
+  tr.injected = true;
   const BlockView* bv = (const BlockView*)blocks;
   for (uint32_t i = 0; i < tr.blk.size(); ++i) {
     tr.blk[i].res = bv[i].res; tr.blk[i].owner = bv[i].owner; tr.blk[i].pos = bv[i].pos;

@@ -18,7 +18,8 @@ LIB = os.path.join(ROOT, "oracle", "librkc_oracle.so")
 TESTS = ["tests/test_oracle_decisions.py", "tests/test_oracle_paper.py",
          "tests/test_oracle_litmus.py", "tests/test_oracle_bruteforce.py",
          "tests/test_oracle_prefix_hits.py", "tests/test_oracle_random.py",
-         "tests/test_oracle_reserve.py", "tests/test_oracle_conformance.py"]
+         "tests/test_oracle_reserve.py", "tests/test_oracle_conformance.py",
+         "tests/test_oracle_readings.py"]
 
 # (name, old, new): each `old` must occur exactly once in the oracle source
 MUTANTS = [
@@ -58,6 +59,16 @@ MUTANTS = [
     ("admission reserve under every lowering", "    if (cfg.lowering != LOW_CONTRACT) return 0;\n    uint64_t r = 0;",
      "    uint64_t r = 0;"),
     ("admission reserve boundary <", "    if (Rv + A <= cfg.U) return true;", "    if (Rv + A < cfg.U) return true;"),
+    ("head-first stamps on insert (G1)", "b.res = B_CACHED; b.owner = (uint8_t)o; b.pos = i; b.seq = base + (n - 1 - i);",
+     "b.res = B_CACHED; b.owner = (uint8_t)o; b.pos = i; b.seq = base + i;"),
+    ("head-first stamps on complete (G1)", "b.seq = base + (full - 1 - b.pos); }",
+     "b.seq = base + b.pos; }"),
+    ("soft claims not evicted last (G6)",
+     "if (m == M_SOFT || (cfg.lowering == LOW_SOFT && obligated(m))) return 2;",
+     "if (m == M_SOFT || (cfg.lowering == LOW_SOFT && obligated(m))) return 1;"),
+    ("auto-demotion from the highest slot (G10)",
+     "        if (live_claim(c) && clm[c].mode == M_DEMOTABLE) {\n          uint32_t pc = protected_of_claim(c);\n          if (pc > 0) { dm.push_back(c); g.push_back(pc); }",
+     "        if (live_claim(c) && clm[c].mode == M_DEMOTABLE) {\n          uint32_t pc = protected_of_claim(c);\n          if (pc > 0) { dm.insert(dm.begin(), c); g.insert(g.begin(), pc); }"),
     ("shortfall off by one", "const uint32_t shortfall = (uint32_t)((uint64_t)P + A - U);",
      "const uint32_t shortfall = (uint32_t)((uint64_t)P + A - U - 1);"),
 ]
