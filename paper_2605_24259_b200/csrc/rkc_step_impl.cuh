@@ -1950,17 +1950,10 @@ __device__ __forceinline__ void run_item(const StepArgs& args, const uint32_t* t
   // hot header (lanes 0..15), the request record, the claim / object tables.
   const bool rq_op = (kind == OP_ADMIT || kind == OP_ADVANCE || kind == OP_COMPLETE ||
                       kind == OP_HIT_ADMIT) && a < p.Q;
-#ifndef RKC_BIG_PRELOAD
-#define RKC_BIG_PRELOAD 0
-#endif
-  // big pools: an ADVANCE's allocation needs the claim / object tables before its
-  // first crew pass (victim attribution); loading them here, beside the request
-  // record, takes one dependent round trip off the leader's serial path
-  const bool adv_pre = RKC_BIG_PRELOAD && kBig && kind == OP_ADVANCE;
   const bool want_cl = kind == OP_SUBMIT || kind == OP_DEMOTE || kind == OP_TOUCH ||
-                       kind == OP_COMPLETE || kind == OP_INSERT || kind == OP_HIT_ADMIT || adv_pre;
+                       kind == OP_COMPLETE || kind == OP_INSERT || kind == OP_HIT_ADMIT;
   const bool want_ob = kind == OP_SUBMIT || kind == OP_INSERT || kind == OP_COMPLETE ||
-                       kind == OP_TOUCH || kind == OP_HIT_ADMIT || adv_pre;
+                       kind == OP_TOUCH || kind == OP_HIT_ADMIT;
   uint32_t rqv = 0;
   if (rq_op && lane < 8) rqv = __ldcg(p.req + ((size_t)t * p.Q + a) * 8 + lane);
   uint4 c0 = make_uint4(0, 0, 0, 0), c1 = make_uint4(0, 0, 0, 0);
