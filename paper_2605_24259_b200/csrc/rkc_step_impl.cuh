@@ -186,7 +186,14 @@ __device__ __forceinline__ void write_event(uint32_t idx, uint32_t type, uint32_
     e[1] = make_uint4(f0, f1, f2, f3);
   }
 }
+#ifndef RKC_EMIT_INLINE
+#define RKC_EMIT_INLINE 1
+#endif
+#if RKC_EMIT_INLINE
+__device__ __forceinline__ void emit(uint32_t type, uint32_t slot, uint32_t reason,
+#else
 __device__ __noinline__ void emit(uint32_t type, uint32_t slot, uint32_t reason,
+#endif
                                   uint32_t mask, uint32_t f0, uint32_t f1, uint32_t f2, uint32_t f3) {
   const uint32_t n = S.nev;
   if (lane_id() == 0) {
@@ -250,9 +257,28 @@ __device__ __forceinline__ void need_tables(bool claims, bool objs) {
   if (lane == 0) S.flags |= (claims ? F_CLAIMS : 0u) | (objs ? F_OBJS : 0u);
   __syncwarp();
 }
+#ifndef RKC_NEED_INLINE_CHECK
+#define RKC_NEED_INLINE_CHECK 1
+#endif
+#if RKC_NEED_INLINE_CHECK
+// the loaded-already test inline at every call site, the loads out of line
+__device__ __noinline__ void load_claims() { need_tables(true, false); }
+__device__ __noinline__ void load_objs() { need_tables(false, true); }
+__device__ __noinline__ void load_both() { need_tables(true, true); }
+__device__ __forceinline__ void need_claims() { if (!(S.flags & F_CLAIMS)) load_claims(); }
+__device__ __forceinline__ void need_objs() { if (!(S.flags & F_OBJS)) load_objs(); }
+__device__ __forceinline__ void need_both() {
+  const uint32_t f = S.flags & (F_CLAIMS | F_OBJS);
+  if (f == (F_CLAIMS | F_OBJS)) return;
+  if (f == F_CLAIMS) load_objs();
+  else if (f == F_OBJS) load_claims();
+  else load_both();
+}
+#else
 __device__ __noinline__ void need_claims() { need_tables(true, false); }
 __device__ __noinline__ void need_objs() { need_tables(false, true); }
 __device__ __noinline__ void need_both() { need_tables(true, true); }
+#endif
 // pull one trace's block array into L2 ahead of a scan (one 128-B line per lane-iteration)
 __device__ __forceinline__ void prefetch_blocks(const uint32_t* base) {
   for (uint32_t l = lane_id(); l < S.NS / 32; l += 32)
@@ -918,7 +944,7 @@ __device__ __noinline__ bool admit_reserve(uint32_t need, uint32_t requester) {
 // auto-demotion (G10); else explicit refusal / deferral with
 // blocking-claim attribution and the capacity proof.
 // requester: request slot (record in S.rq), or 0xFFFFFFFF for INSERT of `obj`.
-__device__ __noinline__ bool arbitrate(uint32_t need, uint32_t requester, uint32_t obj) {
+__device__ __noinline__ bool arbitrate_slow(uint32_t need, uint32_t requester, uint32_t obj) {
     const uint32_t U = S.h[H_U];
   const uint32_t P = S.h[H_P];
   const uint64_t A = (uint64_t)S.h[H_ALIVE] + need;
@@ -951,14 +977,34 @@ __device__ __noinline__ bool arbitrate(uint32_t need, uint32_t requester, uint32
   return infeasible(resident ? WHY_PROTECTED : WHY_CAPACITY, resident ? S.h[H_BLOCKMASK] : 0u, P, A,
                     requester, obj);
 }
+#ifndef RKC_ARB_FAST
+#define RKC_ARB_FAST 0
+#endif
+// the feasible case (P + A <= U) decided inline; everything else out of line
+__device__ __forceinline__ bool arbitrate(uint32_t need, uint32_t requester, uint32_t obj) {
+  if (RKC_ARB_FAST && (uint64_t)S.h[H_P] + S.h[H_ALIVE] + need <= S.h[H_U]) return true;
+  return arbitrate_slow(need, requester, obj);
+}
 
 // ------------------------------ victim selection ---------------------------
+#ifndef RKC_COUNT_UNROLL
+#define RKC_COUNT_UNROLL 1
+#endif
+constexpr int kCountUnroll = RKC_COUNT_UNROLL;
 __device__ __forceinline__ uint4 key_vec(uint32_t j, bool staged) {
   if (staged) return reinterpret_cast<const uint4*>(S.keys)[j * 32 + lane_id()];
   return __ldcg(reinterpret_cast<const uint4*>(S.key) + j * 32 + lane_id());
 }
+#ifndef RKC_COUNT_INLINE
+#define RKC_COUNT_INLINE 1   // round 2: inlined into the search loop (-2 % per c5 step)
+#endif
+#if RKC_COUNT_INLINE
+#define RKC_COUNT_ATTR __forceinline__
+#else
+#define RKC_COUNT_ATTR __noinline__
+#endif
 template <bool staged>
-__device__ __noinline__ uint32_t count_le(uint32_t T) {
+__device__ RKC_COUNT_ATTR uint32_t count_le(uint32_t T) {
 #if RKC_BIG
   if constexpr (!staged) {
     job_args(T);
@@ -968,7 +1014,9 @@ __device__ __noinline__ uint32_t count_le(uint32_t T) {
 #endif
   uint32_t c = 0;
   const uint32_t nv = S.nv;
-#pragma unroll(staged ? 1 : 4)
+  // staged counting is called ~3.5 times per eviction: unrolling it costs a
+  // few hundred bytes of code against the loop overhead of every probe
+#pragma unroll(staged ? kCountUnroll : 4)
   for (uint32_t j = 0; j < nv; ++j) {
     const uint4 v = key_vec(j, staged);
     c += (v.x <= T) + (v.y <= T) + (v.z <= T) + (v.w <= T);
@@ -1064,8 +1112,16 @@ __device__ __noinline__ void alloc_free(uint32_t k, uint32_t owner, bool insert,
 // class (victims are usually the run of oldest stamps), galloping until a
 // probe overshoots, then interpolation / bisection inside the bracket (keys
 // are unique, so the search ends on an exact count).
+#ifndef RKC_EVICT_INLINE
+#define RKC_EVICT_INLINE 1   // round 2: -1.9 % per c5 step
+#endif
+#if RKC_EVICT_INLINE
+#define RKC_EVICT_ATTR __forceinline__
+#else
+#define RKC_EVICT_ATTR __noinline__
+#endif
 template <bool staged>
-__device__ __noinline__ void alloc_evict(uint32_t k, uint32_t owner, bool insert, uint32_t base) {
+__device__ RKC_EVICT_ATTR void alloc_evict(uint32_t k, uint32_t owner, bool insert, uint32_t base) {
   const uint32_t fr = S.h[H_FREE];
   const uint32_t nv = S.nv;
   const uint32_t lane = lane_id();
@@ -1230,10 +1286,15 @@ __device__ __noinline__ void alloc_evict(uint32_t k, uint32_t owner, bool insert
       __syncwarp();
     }
     drain(listed);
-    // every free block was taken
+    // every free block was taken (staged pools have at most 32 bitmap words:
+    // one store per lane)
     {
       uint32_t* fb = S.fbm;
-      for (uint32_t wi = lane_id(); wi < nv * 4; wi += 32) fb[wi] = 0;
+      if (staged) {
+        if (lane_id() < nv * 4) fb[lane_id()] = 0;
+      } else {
+        for (uint32_t wi = lane_id(); wi < nv * 4; wi += 32) fb[wi] = 0;
+      }
     }
   }
   ord = __reduce_add_sync(kFull, ord);
@@ -1254,7 +1315,14 @@ __device__ __noinline__ void alloc_evict(uint32_t k, uint32_t owner, bool insert
 // alloc(k): take the k smallest (class, key) candidates.
 // insert: blocks become CACHED(obj owner) with tail-first stamps, else
 // ACTIVE(request owner).
+#ifndef RKC_ALLOC_INLINE
+#define RKC_ALLOC_INLINE 1   // round 2: -0.6 % per c5 step
+#endif
+#if RKC_ALLOC_INLINE
+__device__ __forceinline__ void alloc(uint32_t k, uint32_t owner, bool insert,
+#else
 __device__ __noinline__ void alloc(uint32_t k, uint32_t owner, bool insert,
+#endif
                                    uint32_t base) {
   flush_reclass();
   if (insert) need_both();
@@ -1405,7 +1473,14 @@ __device__ __noinline__ void op_hit_admit(const Op op) {
 
 // ADVANCE: one prefill chunk or one decode token (G14); live KV
 // accumulates as ceil(done/16) (Table 8).
+#ifndef RKC_ADVANCE_INLINE
+#define RKC_ADVANCE_INLINE 0
+#endif
+#if RKC_ADVANCE_INLINE
+__device__ __forceinline__ void op_advance(const Op op) {
+#else
 __device__ __noinline__ void op_advance(const Op op) {
+#endif
     if (op.a >= S.Q) return op_error(op, ERR_INVALID_ARG);
   load_request(op.a);
   const uint32_t st = S.rq[RQ_W0] & 0xFFu;
@@ -1679,7 +1754,14 @@ __device__ __noinline__ void post_op() {
   refresh_protected();
 }
 
+#ifndef RKC_FINISH_INLINE
+#define RKC_FINISH_INLINE 1   // round 2 (with RKC_NEED_INLINE_CHECK and RKC_EMIT_INLINE: -2.9 % per c5 step)
+#endif
+#if RKC_FINISH_INLINE
+__device__ __forceinline__ void finish() {
+#else
 __device__ __noinline__ void finish() {
+#endif
     flush_reclass();
   if (S.flags & F_POST) {
     post_op();
