@@ -664,8 +664,16 @@ __device__ __forceinline__ void crew_exit() {}
 
 // reclass pass: rewrite the class bits of every cached block whose owner is
 // marked, from the owner's bound claim; recount the protected blocks.
+#ifndef RKC_RECLASS_INLINE
+#define RKC_RECLASS_INLINE 0
+#endif
+#if RKC_RECLASS_INLINE
+#define RKC_RECLASS_ATTR __forceinline__
+#else
+#define RKC_RECLASS_ATTR __noinline__
+#endif
 template <bool big>
-__device__ __noinline__ void flush_reclass_pass() {
+__device__ RKC_RECLASS_ATTR void flush_reclass_pass() {
   if (!big) prefetch_blocks(S.meta);
   need_both();
   const uint32_t low = lowering();
@@ -978,7 +986,7 @@ __device__ __noinline__ bool arbitrate_slow(uint32_t need, uint32_t requester, u
                     requester, obj);
 }
 #ifndef RKC_ARB_FAST
-#define RKC_ARB_FAST 0
+#define RKC_ARB_FAST 1   // round 2: -1.2 % per c5 step
 #endif
 // the feasible case (P + A <= U) decided inline; everything else out of line
 __device__ __forceinline__ bool arbitrate(uint32_t need, uint32_t requester, uint32_t obj) {
@@ -1343,9 +1351,25 @@ __device__ __forceinline__ uint32_t peak_blocks() {
   return (uint32_t)(((uint64_t)S.rq[RQ_PROMPT] + S.rq[RQ_DECODE] + kBlockTokens - 1) / kBlockTokens);
 }
 
+#ifndef RKC_OPS_INLINE
+#define RKC_OPS_INLINE 0
+#endif
+#if RKC_OPS_INLINE
+#define RKC_OP_ATTR __forceinline__
+#else
+#define RKC_OP_ATTR __noinline__
+#endif
+#ifndef RKC_POST_INLINE
+#define RKC_POST_INLINE 1   // round 2: -0.8 % per c5 step
+#endif
+#if RKC_POST_INLINE
+#define RKC_POST_ATTR __forceinline__
+#else
+#define RKC_POST_ATTR __noinline__
+#endif
 // ------------------------------ ops ----------------------------------------
 // SUBMIT: claim decision (Table 2).
-__device__ __noinline__ void op_submit(const Op op) {
+__device__ RKC_OP_ATTR void op_submit(const Op op) {
     const uint32_t mode = op.c & 0x7Fu;
   const bool mismatch = (op.c & 0x80u) != 0;
   if (op.a >= S.C || op.b >= S.O || mode > M_BEST_EFFORT) return op_error(op, ERR_INVALID_ARG);
@@ -1389,7 +1413,7 @@ __device__ __noinline__ void op_submit(const Op op) {
   flag_set(F_POST);
 }
 
-__device__ __noinline__ void op_admit(const Op op) {
+__device__ RKC_OP_ATTR void op_admit(const Op op) {
     if (op.a >= S.Q || op.b >= S.O || op.c > 1) return op_error(op, ERR_INVALID_ARG);
   load_request(op.a);
   const uint32_t st = S.rq[RQ_W0] & 0xFFu;
@@ -1414,7 +1438,7 @@ __device__ __noinline__ void op_admit(const Op op) {
 // one prompt token is computed, is shared and pinned instead of allocated;
 // the PEAK check asks for the exclusive peak plus the newly pinned blocks
 // that were candidates (pinned blocks are active live KV, counted once).
-__device__ __noinline__ void op_hit_admit(const Op op) {
+__device__ RKC_OP_ATTR void op_hit_admit(const Op op) {
   if (op.a >= S.Q || op.b >= S.O || op.c != 0) return op_error(op, ERR_INVALID_ARG);
   load_request(op.a);
   const uint32_t st = S.rq[RQ_W0] & 0xFFu;
@@ -1474,7 +1498,7 @@ __device__ __noinline__ void op_hit_admit(const Op op) {
 // ADVANCE: one prefill chunk or one decode token (G14); live KV
 // accumulates as ceil(done/16) (Table 8).
 #ifndef RKC_ADVANCE_INLINE
-#define RKC_ADVANCE_INLINE 0
+#define RKC_ADVANCE_INLINE 1   // round 2: -1.4 % per c5 step
 #endif
 #if RKC_ADVANCE_INLINE
 __device__ __forceinline__ void op_advance(const Op op) {
@@ -1518,7 +1542,14 @@ __device__ __noinline__ void op_advance(const Op op) {
 // COMPLETE: future reusable admission is separate from active allocation
 // (Table 7); only full blocks become reusable (G16).
 template <bool big>
-__device__ __noinline__ void op_complete(const Op op) {
+#ifndef RKC_COMPLETE_INLINE
+#define RKC_COMPLETE_INLINE 0
+#endif
+#if RKC_COMPLETE_INLINE
+__device__ __forceinline__ void op_complete(const Op op) {
+#else
+__device__ RKC_OP_ATTR void op_complete(const Op op) {
+#endif
     if (op.a >= S.Q) return op_error(op, ERR_INVALID_ARG);
   load_request(op.a);
   if ((S.rq[RQ_W0] & 0xFFu) != R_RUNNING) return op_error(op, ERR_UNKNOWN_REQUEST);
@@ -1604,7 +1635,7 @@ __device__ __noinline__ void op_complete(const Op op) {
 }
 
 // INSERT: resident insertion through the ordinary allocation path (G17).
-__device__ __noinline__ void op_insert(const Op op) {
+__device__ RKC_OP_ATTR void op_insert(const Op op) {
     if (op.a >= S.O) return op_error(op, ERR_INVALID_ARG);
   need_objs();
   const uint32_t ow = S.obj0[op.a];
@@ -1627,7 +1658,7 @@ __device__ __noinline__ void op_insert(const Op op) {
 }
 
 // DEMOTE: claim_demoted before post-release block loss (Table 4).
-__device__ __noinline__ void op_demote(const Op op) {
+__device__ RKC_OP_ATTR void op_demote(const Op op) {
     if (op.a >= S.C) return op_error(op, ERR_INVALID_ARG);
   need_claims();
   const uint32_t st = cl_state(op.a);
@@ -1647,7 +1678,14 @@ __device__ __noinline__ void op_demote(const Op op) {
 // TOUCH: reuse probe of the materialization surface;
 // restamps the leading prefix tail-first (G23).
 template <bool big>
-__device__ __noinline__ void op_touch(const Op op) {
+#ifndef RKC_TOUCH_INLINE
+#define RKC_TOUCH_INLINE 0
+#endif
+#if RKC_TOUCH_INLINE
+__device__ __forceinline__ void op_touch(const Op op) {
+#else
+__device__ RKC_OP_ATTR void op_touch(const Op op) {
+#endif
     if (op.a >= S.O) return op_error(op, ERR_INVALID_ARG);
   need_objs();
   const uint32_t ow = S.obj0[op.a];
@@ -1727,7 +1765,7 @@ __device__ __noinline__ void expiry() {
 // post-op predicate pass: accepted -> materialized when leading >= R
 // (P:1038-1041); materialized -> harmed when the predicate breaks without a
 // prior release (Table 4, G5)
-__device__ __noinline__ void post_op() {
+__device__ RKC_POST_ATTR void post_op() {
   need_both();
     const bool lc = lane_id() < S.C;
   const uint32_t w0 = S.cl[lane_id()][0];
