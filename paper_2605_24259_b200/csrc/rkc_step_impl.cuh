@@ -61,7 +61,11 @@ constexpr int kCrewUnroll = RKC_CREW_UNROLL;  // block vectors in flight per lan
 #endif
 constexpr uint32_t kObjMax = RKC_OMAX;
 
-enum : uint32_t { F_CLAIMS = 1, F_OBJS = 2, F_POST = 4, F_CLAIMS_CHANGED = 8, F_HDR = 16, F_RQ = 32 };
+enum : uint32_t { F_CLAIMS = 1, F_OBJS = 2, F_POST = 4, F_CLAIMS_CHANGED = 8, F_HDR = 16, F_RQ = 32,
+                  F_RC = 64 /* some object is marked for the reclass pass (S.rc) */ };
+#ifndef RKC_RC_FLAG
+#define RKC_RC_FLAG 1   // round 2: one flag test instead of four words (-0.7 % per c5 step)
+#endif
 
 struct alignas(16) Warp {      // the warp's shared memory (one warp per CTA)
   // per-trace base pointers and pool dims, set at kernel entry
@@ -289,11 +293,16 @@ __device__ __forceinline__ void mark_obj_dirty(uint32_t o) {
   __syncwarp();
 }
 __device__ __forceinline__ void mark_reclass(uint32_t o) {
-  if (lane_id() == 0) S.rc[o >> 5] |= 1u << (o & 31u);
+  if (lane_id() == 0) { S.rc[o >> 5] |= 1u << (o & 31u); if (RKC_RC_FLAG) S.flags |= F_RC; }
   __syncwarp();
 }
 __device__ __forceinline__ void mark_reclass_lanes(bool pred, uint32_t o) {
   if (pred) atomicOr(&S.rc[o >> 5], 1u << (o & 31u));
+  if (RKC_RC_FLAG) {
+    const bool any = __any_sync(kFull, pred);
+    __syncwarp();
+    if (any && lane_id() == 0) S.flags |= F_RC;
+  }
   __syncwarp();
 }
 __device__ __forceinline__ bool in_reclass(uint32_t o) {
@@ -739,11 +748,12 @@ __device__ RKC_RECLASS_ATTR void flush_reclass_pass() {
   __syncwarp();
   claims_dirty(ch);
   if (lane_id() < 4) S.rc[lane_id()] = 0;
+  if (RKC_RC_FLAG && lane_id() == 0) S.flags &= ~F_RC;
   __syncwarp();
   refresh_protected();
 }
 __device__ __forceinline__ void flush_reclass() {
-  if (S.rc[0] | S.rc[1] | S.rc[2] | S.rc[3]) {
+  if (RKC_RC_FLAG ? (S.flags & F_RC) != 0 : (S.rc[0] | S.rc[1] | S.rc[2] | S.rc[3]) != 0) {
     flush_reclass_pass<kBig>();
   }
 }
