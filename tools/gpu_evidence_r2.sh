@@ -10,6 +10,7 @@ timeout 900 python bench.py > $OUT/bench_c5.json 2> $OUT/bench_c5.err; echo "rc=
 timeout 900 python bench.py --config c3 > $OUT/bench_c3.json 2> $OUT/bench_c3.err; echo "rc=$?" >> $OUT/bench_c3.err
 timeout 900 python bench.py --config c6 > $OUT/bench_c6.json 2> $OUT/bench_c6.err; echo "rc=$?" >> $OUT/bench_c6.err
 timeout 1500 python bench.py --config c4 > $OUT/bench_c4.json 2> $OUT/bench_c4.err; echo "rc=$?" >> $OUT/bench_c4.err
+timeout 900 python bench.py --config c8 > $OUT/bench_c8.json 2> $OUT/bench_c8.err; echo "rc=$?" >> $OUT/bench_c8.err
 timeout 600 python bench.py --impl reference > $OUT/bench_reference.json 2> $OUT/bench_reference.err; echo "rc=$?" >> $OUT/bench_reference.err
 timeout 2400 python tests/run_parity_1m.py --single-pool --chunk 50000 > $OUT/parity_1m_single_pool.log 2>&1; echo "rc=$?" >> $OUT/parity_1m_single_pool.log
 CS=/usr/local/cuda/bin/compute-sanitizer
@@ -17,3 +18,6 @@ timeout 1500 $CS --tool memcheck --print-limit 20 python -m pytest tests/test_gp
 timeout 900 $CS --tool racecheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/sanitize_racecheck.log 2>&1; echo "rc=$?" >> $OUT/sanitize_racecheck.log
 timeout 900 $CS --tool synccheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/sanitize_synccheck.log 2>&1; echo "rc=$?" >> $OUT/sanitize_synccheck.log
 ls -la $OUT
+NCU=/usr/local/cuda/bin/ncu
+timeout 1200 $NCU --set full --clock-control none --import-source on -k regex:"rkc_(step|light|step_overflow)_kernel" -s 384 -c 3 -o $OUT/prof_c5 python tools/profile_run.py --traces 1000000 > $OUT/prof_c5.log 2>&1
+timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_c5.csv python tools/profile_run.py --traces 1000000 > $OUT/launches_c5.log 2>&1
