@@ -13,10 +13,7 @@ timeout 1500 python bench.py --config c4 > $OUT/bench_c4.json 2> $OUT/bench_c4.e
 timeout 900 python bench.py --config c8 > $OUT/bench_c8.json 2> $OUT/bench_c8.err; echo "rc=$?" >> $OUT/bench_c8.err
 timeout 600 python bench.py --impl reference > $OUT/bench_reference.json 2> $OUT/bench_reference.err; echo "rc=$?" >> $OUT/bench_reference.err
 timeout 2400 python tests/run_parity_1m.py --single-pool --chunk 50000 > $OUT/parity_1m_single_pool.log 2>&1; echo "rc=$?" >> $OUT/parity_1m_single_pool.log
-CS=/usr/local/cuda/bin/compute-sanitizer
-timeout 1500 $CS --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_parity.py tests/test_gpu_boundary.py -x -q -k "paper_litmus or pool_sizes or slot_stress_parity_all_slots or c4_subset or reserve or drain or staging or malformed or leading or spec" > $OUT/sanitize_memcheck.log 2>&1; echo "rc=$?" >> $OUT/sanitize_memcheck.log
-timeout 900 $CS --tool racecheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/sanitize_racecheck.log 2>&1; echo "rc=$?" >> $OUT/sanitize_racecheck.log
-timeout 900 $CS --tool synccheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/sanitize_synccheck.log 2>&1; echo "rc=$?" >> $OUT/sanitize_synccheck.log
+# compute-sanitizer is closed on this GPU pool (runs under it left GPUs needing a reset)
 ls -la $OUT
 NCU=/usr/local/cuda/bin/ncu
 timeout 1200 $NCU --set full --clock-control none --import-source on -k regex:"rkc_(step|light|step_overflow)_kernel" -s 384 -c 3 -o $OUT/prof_c5 python tools/profile_run.py --traces 1000000 > $OUT/prof_c5.log 2>&1
