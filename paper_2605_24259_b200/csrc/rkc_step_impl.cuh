@@ -61,6 +61,31 @@ constexpr int kCrewUnroll = RKC_CREW_UNROLL;  // block vectors in flight per lan
 #endif
 constexpr uint32_t kObjMax = RKC_OMAX;
 
+#ifndef RKC_ITEMS_PER_CTA
+#define RKC_ITEMS_PER_CTA 1   // small pools: heavy items per one-warp CTA (1 or 2)
+#endif
+#ifndef RKC_RUN_ITEM_ATTR
+#if RKC_ITEMS_PER_CTA == 2
+#define RKC_RUN_ITEM_ATTR __noinline__   // one call per item (an inlined loop body spills)
+#else
+#define RKC_RUN_ITEM_ATTR __forceinline__
+#endif
+#endif
+#ifndef RKC_TICKET_REVERSE
+#define RKC_TICKET_REVERSE 0   // items of a bucket in reverse ticket order (latest light-pass traces first)
+#endif
+#ifndef RKC_LIGHT_WARP_ATOMICS
+#define RKC_LIGHT_WARP_ATOMICS 0
+#endif
+#ifndef RKC_LIGHT_RANKED
+#define RKC_LIGHT_RANKED 1   // free-only takes: one rank per lane instead of a bit loop per word
+#endif
+#ifndef RKC_FREE_RANKED
+#define RKC_FREE_RANKED 0    // the same in the step kernel's free-only allocation
+#endif
+#ifndef RKC_LIGHT_MIN_CTAS
+#define RKC_LIGHT_MIN_CTAS 10   // 48 registers: 10 light CTAs per SM
+#endif
 enum : uint32_t { F_CLAIMS = 1, F_OBJS = 2, F_POST = 4, F_CLAIMS_CHANGED = 8, F_HDR = 16, F_RQ = 32,
                   F_RC = 64 /* some object is marked for the reclass pass (S.rc) */ };
 #ifndef RKC_RC_FLAG
@@ -386,6 +411,15 @@ __device__ __forceinline__ void crew_bar() {
 }
 __device__ __forceinline__ uint32_t crew_j0(uint32_t w) { return S.nv * w / kCrew; }
 
+// L2 prefetch of the line RKC_CREW_PF vectors ahead in a crew pass (one
+// prefetch per 128-B line: lanes 0, 8, 16, 24); no registers held
+#ifndef RKC_CREW_PF
+#define RKC_CREW_PF 4   // round 2: c4 702 -> 494 us per lockstep step
+#endif
+__device__ __forceinline__ void crew_pf(const uint4* base, uint32_t j, uint32_t j1) {
+  if (RKC_CREW_PF > 0 && (lane_id() & 7u) == 0 && j + RKC_CREW_PF < j1)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (j + RKC_CREW_PF) * 32 + lane_id()));
+}
 // one job's slice for warp w (lane = lane_id()); arguments in S.job[1..7]
 __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
   const uint32_t lane = lane_id();
@@ -401,6 +435,7 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
       uint32_t md = kFull;
 #pragma unroll(kCrewUnroll)
       for (uint32_t j = j0; j < j1; ++j) {
+        crew_pf(key4, j, j1);
         const uint4 v = __ldcg(key4 + j * 32 + lane);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -417,6 +452,7 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
       const uint32_t T = S.job[1];
 #pragma unroll(kCrewUnroll)
       for (uint32_t j = j0; j < j1; ++j) {
+        crew_pf(key4, j, j1);
         const uint4 v = __ldcg(key4 + j * 32 + lane);
         r0 += (v.x <= T) + (v.y <= T) + (v.z <= T) + (v.w <= T);
       }
@@ -428,6 +464,7 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
       uint32_t m2 = kFull;
 #pragma unroll(kCrewUnroll)
       for (uint32_t j = j0; j < j1; ++j) {
+        crew_pf(key4, j, j1);
         const uint4 v = __ldcg(key4 + j * 32 + lane);
         m2 = min(min(m2, v.x - kC2), min(v.y - kC2, min(v.z - kC2, v.w - kC2)));
       }
@@ -442,6 +479,7 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
       for (uint32_t v = 0; v < w; ++v) rank += S.red[v][0];
       const uint32_t end = rank + S.red[w][0];
       for (uint32_t j = j0; j < j1 && rank < end; ++j) {
+        crew_pf(key4, j, j1);
         const uint4 v = __ldcg(key4 + j * 32 + lane);
         const uint32_t tb = (v.x <= T ? 1u : 0u) | (v.y <= T ? 2u : 0u) | (v.z <= T ? 4u : 0u) |
                             (v.w <= T ? 8u : 0u);
@@ -486,6 +524,7 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
       const uint32_t rq = S.job[1];
 #pragma unroll(kCrewUnroll)
       for (uint32_t j = j0; j < j1; ++j) {
+        crew_pf(meta4, j, j1);
         const uint4 mv = __ldcg(meta4 + j * 32 + lane);
         uint32_t nib = 0;
 #pragma unroll
@@ -513,6 +552,7 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
       const uint32_t seq_base = S.job[6];
 #pragma unroll(kCrewUnroll)
       for (uint32_t j = j0; j < j1; ++j) {
+        crew_pf(meta4, j, j1);
         const uint4 mv = __ldcg(meta4 + j * 32 + lane);
         uint32_t nib = 0;
 #pragma unroll
@@ -541,6 +581,7 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
       const uint32_t ob = S.job[1], L = S.job[2], seq_base = S.job[3];
 #pragma unroll(kCrewUnroll)
       for (uint32_t j = j0; j < j1; ++j) {
+        crew_pf(meta4, j, j1);
         const uint4 mv = __ldcg(meta4 + j * 32 + lane);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -556,6 +597,7 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
     case JOB_RECLASS: {  // class bits of the marked objects' cached blocks (S.lim3 / S.lim2 / S.cnt3)
 #pragma unroll(kCrewUnroll)
       for (uint32_t j = j0; j < j1; ++j) {
+        crew_pf(meta4, j, j1);
         const uint4 mv = __ldcg(meta4 + j * 32 + lane);
         bool any = false;
 #pragma unroll
@@ -1042,6 +1084,27 @@ __device__ RKC_COUNT_ATTR uint32_t count_le(uint32_t T) {
   return __reduce_add_sync(kFull, c);
 }
 
+// Staged pools (round 2): the counting probe also records which of the lane's
+// 32 staged keys are <= T (bit 4j + e for block (j*32 + lane)*4 + e), so the
+// probe that hits the exact count hands the taken set to the apply step
+// without a second pass over the keys.
+#ifndef RKC_MASK_APPLY
+#define RKC_MASK_APPLY 1
+#endif
+__device__ __forceinline__ uint32_t count_mask(uint32_t T, uint32_t& M) {
+  const uint32_t nv = S.nv;
+  uint32_t mk = 0;
+#pragma unroll 1
+  for (uint32_t j = 0; j < nv; ++j) {
+    const uint4 v = reinterpret_cast<const uint4*>(S.keys)[j * 32 + lane_id()];
+    const uint32_t nib = (v.x <= T ? 1u : 0u) | (v.y <= T ? 2u : 0u) | (v.z <= T ? 4u : 0u) |
+                         (v.w <= T ? 8u : 0u);
+    mk |= nib << (4 * j);
+  }
+  M = mk;
+  return __reduce_add_sync(kFull, __popc(mk));
+}
+
 // smallest class-2 (soft) key: d2 = key - 2^31 maps class 2 to [0, 2^30) below
 // every other class (rare path: class 1 cannot cover the shortfall)
 template <bool staged>
@@ -1098,7 +1161,35 @@ __device__ __noinline__ void alloc_free(uint32_t k, uint32_t owner, bool insert,
     const uint32_t Sc = warp_incl_scan(c, lane_id());
     const uint32_t before = acc + Sc - c;
     const uint32_t take = before >= k ? 0u : min(c, k - before);
+#if RKC_FREE_RANKED
+    // rank-parallel (as in the light pass): rank r of this chunk -> lane r % 32
+    if (take > 0) fbm[wi] = word & ~(take == c ? word : word & ((1u << nth_set_bit(word, take + 1)) - 1u));
+    const uint32_t tot = __shfl_sync(kFull, Sc, 31);
+    const uint32_t ntake = min(tot, k - acc);
+    for (uint32_t r0 = 0; r0 < ntake; r0 += 32) {
+      const uint32_t rr = r0 + lane_id();
+      uint32_t sl = 0;
+#pragma unroll
+      for (uint32_t b = 16; b >= 1; b >>= 1)
+        if (__shfl_sync(kFull, Sc, sl + b - 1) <= rr) sl += b;
+      const uint32_t ws = __shfl_sync(kFull, word, sl), bs = __shfl_sync(kFull, Sc - c, sl);
+      if (rr < ntake) {
+        const uint32_t bb = (w0 + sl) * 32 + nth_set_bit(ws, rr - bs + 1);
+        const uint32_t pos = base + acc + rr;
+        if (insert) {
+          const uint32_t cls = pos < l3 ? 3u : (pos < l2 ? 2u : 1u);
+          key[bb] = (cls << kClassShift) | (seq_base + (k - 1 - pos));
+          meta[bb] = meta_make(kResCached, owner, pos);
+        } else {
+          key[bb] = kKeyActive;
+          meta[bb] = meta_make(kResActive, owner, pos);
+        }
+      }
+    }
+    if (false) {
+#else
     if (take > 0) {
+#endif
       uint32_t tw = take == c ? word : word & ((1u << nth_set_bit(word, take + 1)) - 1u);
       fbm[wi] = word & ~tw;
       uint32_t r = before;
@@ -1158,9 +1249,9 @@ __device__ RKC_EVICT_ATTR void alloc_evict(uint32_t k, uint32_t owner, bool inse
       md = min(md, d);
     }
   };
+  uint4 kv[kStageMax / 128];
   if (staged) {
     // issue every key load and the claim / object table loads together
-    uint4 kv[kStageMax / 128];
 #pragma unroll
     for (uint32_t j = 0; j < kStageMax / 128; ++j)
       if (j < nv) kv[j] = __ldcg(key4 + j * 32 + lane);
@@ -1200,6 +1291,29 @@ __device__ RKC_EVICT_ATTR void alloc_evict(uint32_t k, uint32_t owner, bool inse
   // is the same set {key <= T} whatever the probe sequence (keys are unique)
   const uint32_t lo0 = lo, clo0 = clo;
   uint32_t bi = 0, last_d = 0;
+  uint32_t M = 0;  // staged: this lane's taken keys at the last probe (count_mask)
+#ifndef RKC_PROBE_REG
+#define RKC_PROBE_REG 1   // round 2: the first probe from the staging registers
+#endif
+  // staged, class-1 case: the first (dense) probe counted from the key
+  // registers of the staging load (no shared-memory pass)
+  uint32_t pre_cm = 0xFFFFFFFFu;
+  if constexpr (staged && RKC_MASK_APPLY && RKC_PROBE_REG) {
+    if (k - fr <= c1) {
+      const uint32_t m0 = (uint32_t)min((uint64_t)lo + (k - clo), (uint64_t)top);
+      uint32_t mk = 0;
+#pragma unroll
+      for (uint32_t j = 0; j < kStageMax / 128; ++j) {
+        if (j < nv) {
+          const uint4 v = kv[j];
+          mk |= ((v.x <= m0 ? 1u : 0u) | (v.y <= m0 ? 2u : 0u) | (v.z <= m0 ? 4u : 0u) |
+                 (v.w <= m0 ? 8u : 0u)) << (4 * j);
+        }
+      }
+      M = mk;
+      pre_cm = __reduce_add_sync(kFull, __popc(mk));
+    }
+  }
   for (uint32_t it = 0;; ++it) {
     uint32_t m;
     if (!bracket) {
@@ -1222,7 +1336,9 @@ __device__ RKC_EVICT_ATTR void alloc_evict(uint32_t k, uint32_t owner, bool inse
       m = max(m, lo + 1);
       m = min(m, hi - 1);
     }
-    const uint32_t cm = count_le<staged>(m);
+    const uint32_t cm = (staged && RKC_MASK_APPLY)
+                            ? ((it == 0 && pre_cm != 0xFFFFFFFFu) ? pre_cm : count_mask(m, M))
+                            : count_le<staged>(m);
     if (cm == k) { T = m; break; }
     if (cm < k) { lo = m; clo = cm; }
     else { hi = m; chi = cm; bracket = true; }
@@ -1253,7 +1369,65 @@ __device__ RKC_EVICT_ATTR void alloc_evict(uint32_t k, uint32_t owner, bool inse
     if (lane_id() == 0) { ord = crew_sum(1); rel = crew_sum(2); clm = crew_sum(3); }
   } else
 #endif
-  {
+  if constexpr (staged && RKC_MASK_APPLY) {
+    // ranks in block-id order (G24): vector j, then lane, then element.  Per
+    // vector, the lanes' taken counts (<= 4 each, <= 128 per vector) are
+    // scanned as bytes of two words (even / odd vectors) in one warp scan.
+    const uint32_t lane = lane_id();
+    uint32_t x = M - ((M >> 1) & 0x55555555u);
+    x = (x & 0x33333333u) + ((x >> 2) & 0x33333333u);  // nibble j: taken keys of vector j
+    const uint32_t A = x & 0x0F0F0F0Fu, B = (x >> 4) & 0x0F0F0F0Fu;
+    uint32_t Ai = A, Bi = B;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t ua = __shfl_up_sync(kFull, Ai, d), ub = __shfl_up_sync(kFull, Bi, d);
+      if (lane >= (uint32_t)d) { Ai += ua; Bi += ub; }
+    }
+    const uint32_t At = __shfl_sync(kFull, Ai, 31), Bt = __shfl_sync(kFull, Bi, 31);
+    const uint32_t Ae = Ai - A, Be = Bi - B;
+    __syncwarp();  // every lane's last probe has read the staged keys the list overwrites
+    uint32_t vb = 0;
+#pragma unroll 1
+    for (uint32_t j = 0; j < nv; ++j) {
+      const uint32_t sh = 8 * (j >> 1);
+      uint32_t nib = (M >> (4 * j)) & 15u;
+      uint32_t r = vb + ((((j & 1u) ? Be : Ae) >> sh) & 0xFFu);
+      while (nib) {
+        list[r++] = block_of(j, __ffs(nib) - 1);
+        nib &= nib - 1;
+      }
+      vb += (((j & 1u) ? Bt : At) >> sh) & 0xFFu;
+    }
+    __syncwarp();
+    // one taken block per lane: FREE ones (meta residency FREE) are just
+    // taken; cached ones are victims, attributed by their object's claim
+#pragma unroll 1
+    for (uint32_t i = lane; i < k; i += 32) {
+      const uint32_t bb = list[i];
+      const uint32_t pos = base + i;
+      const uint32_t m = __ldcg(meta + bb);
+      if (meta_res(m) == kResCached) {
+        const uint32_t o = meta_owner(m);
+        const uint32_t cc = obj_claim(S.obj0[o]);
+        const uint32_t st = cc < 32 ? cl_state(cc) : C_EMPTY;
+        if (st == C_DEMOTED || st == C_EXPIRED) ++rel;
+        else if (st == C_ACCEPTED || st == C_MATERIALIZED) ++clm;
+        else ++ord;
+        atomicMin(&S.lead[o], meta_pos(m));
+        atomicOr(&S.objdirty[o >> 5], 1u << (o & 31u));
+      }
+      if (insert) {
+        const uint32_t cls = pos < l3 ? 3u : (pos < l2 ? 2u : 1u);
+        key[bb] = (cls << kClassShift) | (seq_base + (k - 1 - pos));
+        meta[bb] = meta_make(kResCached, owner, pos);
+      } else {
+        key[bb] = kKeyActive;
+        meta[bb] = meta_make(kResActive, owner, pos);
+      }
+    }
+    __syncwarp();
+    if (lane < nv * 4) S.fbm[lane] = 0;  // every free block was taken
+  } else {
     uint32_t listed = 0, done_pos = 0;
     auto drain = [&](uint32_t n) {
 #pragma unroll 1
@@ -1883,9 +2057,10 @@ __device__ __forceinline__ uint32_t bucket_of(uint32_t kind) {
 #define RKC_LIGHT_THREADS 128
 #endif
 constexpr uint32_t kLightThreads = RKC_LIGHT_THREADS;
+
 // heavy-trace ticket: op (4 words), hot header words 0..11 (word 10 <- the trace id)
 constexpr uint32_t kTicketWords = 16u;
-__global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_constant__ StepArgs args) {
+__global__ void __launch_bounds__(kLightThreads, RKC_LIGHT_MIN_CTAS) rkc_light_kernel(const __grid_constant__ StepArgs args) {
   const PoolDev& p = args.p;
   const uint32_t step = args.step;
   uint32_t* cnt = p.bcnt + (step & 1u) * 8;
@@ -1997,11 +2172,35 @@ __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_c
       uint32_t* fbm = p.fbm + (size_t)tt * (p.NS / 32);
       const uint32_t word = words[q];
       const uint32_t c = __popc(word);
-      const uint32_t before = warp_incl_scan(c, lane) - c;
+      const uint32_t incl = warp_incl_scan(c, lane);
+      const uint32_t before = incl - c;
       const uint32_t take = before >= need ? 0u : min(c, need - before);
       if (take > 0) {
-        uint32_t tw = take == c ? word : word & ((1u << nth_set_bit(word, take + 1)) - 1u);
+        const uint32_t tw = take == c ? word : word & ((1u << nth_set_bit(word, take + 1)) - 1u);
         fbm[lane] = word & ~tw;
+      }
+#if RKC_LIGHT_RANKED
+      // rank-parallel: rank r (block at position live + r) goes to lane r % 32;
+      // its bitmap word is the first whose inclusive count exceeds r (the taken
+      // blocks of one allocation are usually a run inside one or two words)
+      uint32_t* key = p.key + (size_t)tt * p.NS;
+      uint32_t* meta = p.meta + (size_t)tt * p.NS;
+      for (uint32_t r0 = 0; r0 < need; r0 += 32) {
+        const uint32_t r = r0 + lane;
+        uint32_t sl = 0;
+#pragma unroll
+        for (uint32_t b = 16; b >= 1; b >>= 1)
+          if (__shfl_sync(kFull, incl, sl + b - 1) <= r) sl += b;
+        const uint32_t ws = __shfl_sync(kFull, word, sl & 31u), bs = __shfl_sync(kFull, before, sl & 31u);
+        if (r < need) {
+          const uint32_t b = sl * 32 + nth_set_bit(ws, r - bs + 1);
+          meta[b] = meta_make(kResActive, owner, live + r);
+          key[b] = kKeyActive;
+        }
+      }
+#else
+      if (take > 0) {
+        uint32_t tw = take == c ? word : word & ((1u << nth_set_bit(word, take + 1)) - 1u);
         uint32_t* key = p.key + (size_t)tt * p.NS;
         uint32_t* meta = p.meta + (size_t)tt * p.NS;
         for (uint32_t r = live + before; tw; tw &= tw - 1, ++r) {
@@ -2010,6 +2209,7 @@ __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_c
           key[b] = kKeyActive;
         }
       }
+#endif
       }
     }
     // bucket ranks: warp match -> CTA shared counts -> one global atomic per bucket per CTA
@@ -2017,6 +2217,12 @@ __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_c
     const uint32_t grp = __match_any_sync(kFull, bk);
     const uint32_t leader = __ffs(grp) - 1;
     uint32_t off = 0;
+#if RKC_LIGHT_WARP_ATOMICS
+    // one global atomic per (warp, bucket): no CTA barrier
+    if (lane == leader && heavy) off = atomicAdd(cnt + bk, __popc(grp));
+    off = __shfl_sync(kFull, off, leader);
+    const uint32_t cbase = 0;
+#else
     if (lane == leader && heavy) off = atomicAdd(&s_cnt[bk], __popc(grp));
     off = __shfl_sync(kFull, off, leader);
     __syncthreads();
@@ -2026,9 +2232,11 @@ __global__ void __launch_bounds__(kLightThreads) rkc_light_kernel(const __grid_c
       s_cnt[threadIdx.x] = 0;
     }
     __syncthreads();
+    const uint32_t cbase = heavy ? s_base[bk] : 0u;
+#endif
     if (heavy) {  // the ticket: op, header words 0..11 (word 10 <- the trace id)[, request]
       uint4* tk = reinterpret_cast<uint4*>(p.perm) +
-                  (kTicketWords / 4) * ((size_t)bk * p.num_traces + s_base[bk] + off + __popc(grp & lanemask_lt()));
+                  (kTicketWords / 4) * ((size_t)bk * p.num_traces + cbase + off + __popc(grp & lanemask_lt()));
       tk[0] = opw;
       tk[1] = hv0;
       tk[2] = hv1;
@@ -2048,7 +2256,7 @@ __device__ __forceinline__ bool item_trace(const StepArgs& args, uint32_t i, con
 #pragma unroll
   for (uint32_t q = 0; q < 8; ++q) {
     const uint32_t c = cnt[q];
-    if (bk == 8 && i < acc + c) { bk = q; off = i - acc; }
+    if (bk == 8 && i < acc + c) { bk = q; off = RKC_TICKET_REVERSE ? acc + c - 1 - i : i - acc; }
     acc += c;
   }
   if (bk == 8) return false;
@@ -2056,20 +2264,13 @@ __device__ __forceinline__ bool item_trace(const StepArgs& args, uint32_t i, con
   return true;
 }
 
-// one heavy trace-step from its ticket: the warp's whole op path
-__device__ __forceinline__ void run_item(const StepArgs& args, const uint32_t* tk) {
+// one heavy trace-step from its ticket word `tw` (lane l < 16 holds word l of
+// the ticket written by the light pass: the op in words 0..3, header words
+// 0..11 in 4..15, the trace id in place of (unused) header word 10): the
+// warp's whole op path
+__device__ RKC_RUN_ITEM_ATTR void run_item_tw(const StepArgs& args, const uint32_t tw) {
   const uint32_t lane = threadIdx.x & 31u;
-#if RKC_BIG
-  if (threadIdx.x >= 32) {  // crew helpers: block-pass slices until the leader is done
-    crew_helper();
-    return;
-  }
-#endif
   const PoolDev& p = args.p;
-  // the ticket (written by the light pass, read through L1): lane l < 16 holds
-  // word l -- the op in words 0..3, header words 0..11 in 4..15, the trace id
-  // in place of (unused) header word 10
-  const uint32_t tw = lane < kTicketWords ? __ldg(tk + lane) : 0u;
   const uint4 opw = make_uint4(__shfl_sync(kFull, tw, 0), __shfl_sync(kFull, tw, 1),
                                __shfl_sync(kFull, tw, 2), __shfl_sync(kFull, tw, 3));
   const uint32_t t = __shfl_sync(kFull, tw, 14);
@@ -2162,6 +2363,17 @@ __device__ __forceinline__ void run_item(const StepArgs& args, const uint32_t* t
   crew_exit();
 }
 
+__device__ __forceinline__ void run_item(const StepArgs& args, const uint32_t* tk) {
+#if RKC_BIG
+  if (threadIdx.x >= 32) {  // crew helpers: block-pass slices until the leader is done
+    crew_helper();
+    return;
+  }
+#endif
+  const uint32_t lane = threadIdx.x & 31u;
+  run_item_tw(args, lane < kTicketWords ? __ldg(tk + lane) : 0u);
+}
+
 // K1: warp w of CTA b -> the (b * kWarpsPerCta + w)-th trace of the op-kind
 // bucketed order.  Small pools launch CTAs for the first kMainItems(T) items
 // only (the heavy share of a step is about half); the rest, if any, run on
@@ -2179,8 +2391,27 @@ __global__ void __launch_bounds__(kWarpsPerCta * kCrew * 32, kMinCtas)
 rkc_step_kernel(const __grid_constant__ StepArgs args) {
   pdl_wait();
   const uint32_t* tk;
+#if !RKC_BIG && RKC_ITEMS_PER_CTA == 2
+  // two consecutive items per one-warp CTA: the second ticket is loaded
+  // before the first item runs, so its latency hides behind the first item
+  const uint32_t i0 = blockIdx.x * 2;
+  if (!item_trace(args, i0, tk)) return;
+  const uint32_t* tk1;
+  const bool two = item_trace(args, i0 + 1, tk1);
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t tw = lane < kTicketWords ? __ldg(tk + lane) : 0u;
+  const uint32_t tw1 = (two && lane < kTicketWords) ? __ldg(tk1 + lane) : 0u;
+#pragma unroll 1
+  for (uint32_t it = 0;; ++it) {
+    run_item_tw(args, tw);
+    if (it == 1 || !two) break;
+    __syncwarp();
+    tw = tw1;
+  }
+#else
   if (!item_trace(args, blockIdx.x * kWarpsPerCta + (kWarpsPerCta == 1 ? 0u : (threadIdx.x >> 5)), tk)) return;
   run_item(args, tk);
+#endif
 }
 
 #if !RKC_BIG
@@ -2247,7 +2478,7 @@ cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, c
     e = launch_pdl(rkc_step_kernel, (p.num_traces + kWarpsPerCta - 1) / kWarpsPerCta, kWarpsPerCta * kCrew * 32, st, args);
 #else
   if (e == cudaSuccess)
-    e = launch_pdl(rkc_step_kernel, (kMainItems(p.num_traces) + kWarpsPerCta - 1) / kWarpsPerCta, kWarpsPerCta * 32, st, args);
+    e = launch_pdl(rkc_step_kernel, (kMainItems(p.num_traces) + kWarpsPerCta * RKC_ITEMS_PER_CTA - 1) / (kWarpsPerCta * RKC_ITEMS_PER_CTA), kWarpsPerCta * 32, st, args);
   if (e == cudaSuccess) e = launch_pdl(rkc_step_overflow_kernel, kOverflowCtas(p.num_traces), 32, st, args);
 #endif
   return e;
