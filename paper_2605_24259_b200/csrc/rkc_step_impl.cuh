@@ -71,6 +71,25 @@ constexpr uint32_t kObjMax = RKC_OMAX;
 #define RKC_RUN_ITEM_ATTR __forceinline__
 #endif
 #endif
+#ifndef RKC_BCNT_STRIDE
+#define RKC_BCNT_STRIDE 1   // words between the bucket counters (32: one 128-B line each)
+#endif
+constexpr uint32_t kBcntStride = RKC_BCNT_STRIDE;
+#ifndef RKC_CREW_VEC
+#define RKC_CREW_VEC 1   // crew apply / touch: one 16-B read-back per vector instead of one load per block (c4 -10 %)
+#endif
+#ifndef RKC_BIG_PRELOAD
+#define RKC_BIG_PRELOAD 0
+#endif
+#ifndef RKC_SEARCH_F32
+#define RKC_SEARCH_F32 1   // threshold-search probe estimates in fp32 instead of 64-bit integer division
+#endif
+#ifndef RKC_CTR_RED
+#define RKC_CTR_RED 0
+#endif
+#ifndef RKC_TICKET_UNIFORM
+#define RKC_TICKET_UNIFORM 1   // ticket fields as uniform loads instead of per-lane words + shuffles
+#endif
 #ifndef RKC_TICKET_REVERSE
 #define RKC_TICKET_REVERSE 0   // items of a bucket in reverse ticket order (latest light-pass traces first)
 #endif
@@ -196,7 +215,14 @@ __device__ __forceinline__ void flag_set(uint32_t f) {
 }
 __device__ __forceinline__ uint32_t lowering() { return S.h[H_POLICY] & 0xFFu; }
 __device__ __forceinline__ void ctr_add(uint32_t k, uint32_t v) {
+#if RKC_CTR_RED
+  // lane 0's predicated shared-memory reduction: no load / use round trip
+  // (read back only in finish(), after a __syncwarp)
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %0, 0;\n\t@p red.shared.add.u32 [%1], %2;\n\t}"
+               ::"r"(lane_id()), "r"((uint32_t)__cvta_generic_to_shared(&S.ctr[k])), "r"(v) : "memory");
+#else
   if (lane_id() == 0) S.ctr[k] += v;
+#endif
 }
 
 // claim record accessors (slot c)
@@ -487,13 +513,23 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
         const uint32_t cnt = __popc(tb);
         const uint32_t Sc = warp_incl_scan(cnt, lane);
         uint32_t r = rank + Sc - cnt;
+#if RKC_CREW_VEC
+        // the vector's meta words in one 16-B load (not one dependent load per victim)
+        const bool anyv = (tb & 1u && v.x >= kC1) || (tb & 2u && v.y >= kC1) || (tb & 4u && v.z >= kC1) ||
+                          (tb & 8u && v.w >= kC1);
+        const uint4 mvv = anyv ? __ldcg(meta4 + j * 32 + lane) : make_uint4(0, 0, 0, 0);
+#endif
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           if (!((tb >> e) & 1u)) continue;
           const uint32_t bb = block_of(j, e);
           const uint32_t pos = base + r++;
           if (el(v, e) >= kC1) {  // a victim: attributed by its object's claim now (Table 4)
+#if RKC_CREW_VEC
+            const uint32_t m = el(mvv, e);
+#else
             const uint32_t m = __ldcg(meta + bb);
+#endif
             const uint32_t o = meta_owner(m);
             const uint32_t cc = obj_claim(S.obj0[o]);
             const uint32_t st = cc < 32 ? cl_state(cc) : C_EMPTY;
@@ -583,6 +619,22 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
       for (uint32_t j = j0; j < j1; ++j) {
         crew_pf(meta4, j, j1);
         const uint4 mv = __ldcg(meta4 + j * 32 + lane);
+#if RKC_CREW_VEC
+        // matching blocks: the key vector read back in one 16-B load
+        uint32_t hit = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t m = el(mv, e);
+          hit |= (meta_res(m) == kResCached && meta_owner(m) == ob && meta_pos(m) < L) ? 1u << e : 0u;
+        }
+        if (hit) {
+          const uint4 kv = __ldcg(key4 + j * 32 + lane);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if ((hit >> e) & 1u)
+              key[block_of(j, e)] = (el(kv, e) & ~kSeqMask) | (seq_base + (L - 1 - meta_pos(el(mv, e))));
+        }
+#else
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const uint32_t m = el(mv, e);
@@ -591,6 +643,7 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
             key[bb] = (__ldcg(key + bb) & ~kSeqMask) | (seq_base + (L - 1 - meta_pos(m)));
           }
         }
+#endif
       }
       break;
     }
@@ -1319,7 +1372,14 @@ __device__ RKC_EVICT_ATTR void alloc_evict(uint32_t k, uint32_t owner, bool inse
     if (!bracket) {
       if (!staged && it > 0 && clo > clo0) {
         // secant step, but never less than twice the last step (no creeping)
+#if RKC_SEARCH_F32
+        // fp32 estimate (the probe position only steers the search; the
+        // taken set {key <= T} is the same for any probe sequence)
+        const float df = fminf((float)(k - clo) * (float)(lo - lo0) * 1.25f / (float)(clo - clo0), 4.0e9f);
+        uint64_t d = (uint64_t)__float2uint_rz(df) + 1;
+#else
         uint64_t d = ((uint64_t)(k - clo) * (lo - lo0) * 5) / ((uint64_t)(clo - clo0) * 4) + 1;
+#endif
         d = max(d, 2 * (uint64_t)last_d);
         last_d = (uint32_t)min(d, (uint64_t)0xFFFFFFFFu);
         m = (uint32_t)min((uint64_t)lo + d, (uint64_t)top);
@@ -1332,7 +1392,12 @@ __device__ RKC_EVICT_ATTR void alloc_evict(uint32_t k, uint32_t owner, bool inse
     } else {
       const uint32_t span = hi - lo;
       const bool interp = staged ? (it & 1u) != 0 : (bi++ & 1u) == 0;
+#if RKC_SEARCH_F32
+      m = interp ? lo + __float2uint_rz(fminf((float)(k - clo) * (float)span / (float)(chi - clo), (float)span))
+                 : lo + span / 2;
+#else
       m = interp ? lo + (uint32_t)(((uint64_t)(k - clo) * span) / (chi - clo)) : lo + span / 2;
+#endif
       m = max(m, lo + 1);
       m = min(m, hi - 1);
     }
@@ -2063,9 +2128,9 @@ constexpr uint32_t kTicketWords = 16u;
 __global__ void __launch_bounds__(kLightThreads, RKC_LIGHT_MIN_CTAS) rkc_light_kernel(const __grid_constant__ StepArgs args) {
   const PoolDev& p = args.p;
   const uint32_t step = args.step;
-  uint32_t* cnt = p.bcnt + (step & 1u) * 8;
+  uint32_t* cnt = p.bcnt + (step & 1u) * 8 * kBcntStride;
   pdl_wait();
-  if (blockIdx.x == 0 && threadIdx.x < 8) p.bcnt[((step + 1u) & 1u) * 8 + threadIdx.x] = 0;
+  if (blockIdx.x == 0 && threadIdx.x < 8) p.bcnt[(((step + 1u) & 1u) * 8 + threadIdx.x) * kBcntStride] = 0;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t stride = gridDim.x * blockDim.x;
   __shared__ uint32_t s_cnt[8], s_base[8];
@@ -2219,7 +2284,7 @@ __global__ void __launch_bounds__(kLightThreads, RKC_LIGHT_MIN_CTAS) rkc_light_k
     uint32_t off = 0;
 #if RKC_LIGHT_WARP_ATOMICS
     // one global atomic per (warp, bucket): no CTA barrier
-    if (lane == leader && heavy) off = atomicAdd(cnt + bk, __popc(grp));
+    if (lane == leader && heavy) off = atomicAdd(cnt + bk * kBcntStride, __popc(grp));
     off = __shfl_sync(kFull, off, leader);
     const uint32_t cbase = 0;
 #else
@@ -2228,7 +2293,7 @@ __global__ void __launch_bounds__(kLightThreads, RKC_LIGHT_MIN_CTAS) rkc_light_k
     __syncthreads();
     if (threadIdx.x < 8) {
       const uint32_t c = s_cnt[threadIdx.x];
-      s_base[threadIdx.x] = c ? atomicAdd(cnt + threadIdx.x, c) : 0u;
+      s_base[threadIdx.x] = c ? atomicAdd(cnt + threadIdx.x * kBcntStride, c) : 0u;
       s_cnt[threadIdx.x] = 0;
     }
     __syncthreads();
@@ -2247,11 +2312,18 @@ __global__ void __launch_bounds__(kLightThreads, RKC_LIGHT_MIN_CTAS) rkc_light_k
 
 // bucketed item i of this step -> its trace (false past the heavy count)
 __device__ __forceinline__ bool item_trace(const StepArgs& args, uint32_t i, const uint32_t*& tk) {
-  const uint4* cnt4 = reinterpret_cast<const uint4*>(args.p.bcnt + (args.step & 1u) * 8);
   // read-only in this kernel and written by the previous one: the L1 path
   // serves every CTA of an SM after the first (an L2 round trip each before)
+#if RKC_BCNT_STRIDE == 1
+  const uint4* cnt4 = reinterpret_cast<const uint4*>(args.p.bcnt + (args.step & 1u) * 8);
   const uint4 ca = __ldg(cnt4), cb = __ldg(cnt4 + 1);
   const uint32_t cnt[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+#else
+  const uint32_t* cp = args.p.bcnt + (args.step & 1u) * 8 * kBcntStride;
+  uint32_t cnt[8];
+#pragma unroll
+  for (uint32_t q = 0; q < 8; ++q) cnt[q] = __ldg(cp + q * kBcntStride);
+#endif
   uint32_t acc = 0, bk = 8, off = 0;
 #pragma unroll
   for (uint32_t q = 0; q < 8; ++q) {
@@ -2268,23 +2340,22 @@ __device__ __forceinline__ bool item_trace(const StepArgs& args, uint32_t i, con
 // the ticket written by the light pass: the op in words 0..3, header words
 // 0..11 in 4..15, the trace id in place of (unused) header word 10): the
 // warp's whole op path
-__device__ RKC_RUN_ITEM_ATTR void run_item_tw(const StepArgs& args, const uint32_t tw) {
+__device__ RKC_RUN_ITEM_ATTR void run_item_body(const StepArgs& args, const uint4 opw, const uint32_t t,
+                                                const uint32_t hw, const uint32_t next_exp) {
   const uint32_t lane = threadIdx.x & 31u;
   const PoolDev& p = args.p;
-  const uint4 opw = make_uint4(__shfl_sync(kFull, tw, 0), __shfl_sync(kFull, tw, 1),
-                               __shfl_sync(kFull, tw, 2), __shfl_sync(kFull, tw, 3));
-  const uint32_t t = __shfl_sync(kFull, tw, 14);
-  const uint32_t hsh = __shfl_sync(kFull, tw, (lane + 4) & 31u);
-  const uint32_t hw = lane < 10 ? hsh : 0u;  // hot header words 0..9 (10..15 unused)
   const uint32_t kind = opw.x & 0xFFu, a = (opw.x >> 8) & 0xFFu;
   // Issue every load this op is known to need before waiting on any of them:
   // hot header (lanes 0..15), the request record, the claim / object tables.
   const bool rq_op = (kind == OP_ADMIT || kind == OP_ADVANCE || kind == OP_COMPLETE ||
                       kind == OP_HIT_ADMIT) && a < p.Q;
+  // (big pools: an ADVANCE's allocation almost always evicts, and the
+  // eviction needs both tables: loaded here, off the crew's critical path)
+  const bool adv_tables = kBig && RKC_BIG_PRELOAD && kind == OP_ADVANCE;
   const bool want_cl = kind == OP_SUBMIT || kind == OP_DEMOTE || kind == OP_TOUCH ||
-                       kind == OP_COMPLETE || kind == OP_INSERT || kind == OP_HIT_ADMIT;
+                       kind == OP_COMPLETE || kind == OP_INSERT || kind == OP_HIT_ADMIT || adv_tables;
   const bool want_ob = kind == OP_SUBMIT || kind == OP_INSERT || kind == OP_COMPLETE ||
-                       kind == OP_TOUCH || kind == OP_HIT_ADMIT;
+                       kind == OP_TOUCH || kind == OP_HIT_ADMIT || adv_tables;
   uint32_t rqv = 0;
   if (rq_op && lane < 8) rqv = __ldcg(p.req + ((size_t)t * p.Q + a) * 8 + lane);
   uint4 c0 = make_uint4(0, 0, 0, 0), c1 = make_uint4(0, 0, 0, 0);
@@ -2308,14 +2379,17 @@ __device__ RKC_RUN_ITEM_ATTR void run_item_tw(const StepArgs& args, const uint32
     if (scan) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.meta + (size_t)t * p.NS + lane * 32));
     if (sel) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.key + (size_t)t * p.NS + lane * 32));
   }
-  const uint32_t next_exp = __shfl_sync(kFull, hw, H_NEXT_EXPIRY);
   // a NOP with no expiry due changes nothing (fast path)
   if (kind == OP_NOP && args.step < next_exp) {
     crew_exit();
     return;
   }
   if (lane < H_NWORDS) S.h[lane] = hw;
+#if RKC_TICKET_UNIFORM
+  S.ctr[lane] = (lane == K_OPS && kind != OP_NOP) ? 1u : 0u;  // the op counts itself
+#else
   S.ctr[lane] = 0;
+#endif
   if (lane < 4) { S.rc[lane] = 0; S.objdirty[lane] = 0; }
   if (lane < 8) S.rq[lane] = rqv;
   if (want_cl) {
@@ -2345,7 +2419,7 @@ __device__ RKC_RUN_ITEM_ATTR void run_item_tw(const StepArgs& args, const uint32
   __syncwarp();
   Op op{kind, a, (opw.x >> 16) & 0xFFu, opw.x >> 24, opw.y, opw.z, opw.w};
   if (args.step >= next_exp) expiry();
-  if (kind != OP_NOP) ctr_add(K_OPS, 1);
+  if (!RKC_TICKET_UNIFORM && kind != OP_NOP) ctr_add(K_OPS, 1);
   switch (kind) {
     case OP_NOP: break;
     case OP_SUBMIT: op_submit(op); break;
@@ -2363,6 +2437,16 @@ __device__ RKC_RUN_ITEM_ATTR void run_item_tw(const StepArgs& args, const uint32
   crew_exit();
 }
 
+// the ticket as one word per lane (lane l < 16 holds word l), spread by shuffles
+__device__ __forceinline__ void run_item_tw(const StepArgs& args, const uint32_t tw) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint4 opw = make_uint4(__shfl_sync(kFull, tw, 0), __shfl_sync(kFull, tw, 1),
+                               __shfl_sync(kFull, tw, 2), __shfl_sync(kFull, tw, 3));
+  const uint32_t t = __shfl_sync(kFull, tw, 14);
+  const uint32_t hsh = __shfl_sync(kFull, tw, (lane + 4) & 31u);
+  const uint32_t hw = lane < 10 ? hsh : 0u;  // hot header words 0..9 (10..15 unused)
+  run_item_body(args, opw, t, hw, __shfl_sync(kFull, hw, H_NEXT_EXPIRY));
+}
 __device__ __forceinline__ void run_item(const StepArgs& args, const uint32_t* tk) {
 #if RKC_BIG
   if (threadIdx.x >= 32) {  // crew helpers: block-pass slices until the leader is done
@@ -2371,7 +2455,18 @@ __device__ __forceinline__ void run_item(const StepArgs& args, const uint32_t* t
   }
 #endif
   const uint32_t lane = threadIdx.x & 31u;
+#if RKC_TICKET_UNIFORM
+  // the op (words 0..3) and words 12..15 {next expiry, event count, trace, -}
+  // as warp-uniform 16-B loads, header words 0..9 one per lane: independent
+  // loads, no shuffles
+  const uint4* tk4 = reinterpret_cast<const uint4*>(tk);
+  const uint4 opw = __ldg(tk4);
+  const uint4 tail = __ldg(tk4 + 3);
+  const uint32_t hw = lane < 10 ? __ldg(tk + 4 + lane) : 0u;
+  run_item_body(args, opw, tail.z, hw, tail.x);
+#else
   run_item_tw(args, lane < kTicketWords ? __ldg(tk + lane) : 0u);
+#endif
 }
 
 // K1: warp w of CTA b -> the (b * kWarpsPerCta + w)-th trace of the op-kind
