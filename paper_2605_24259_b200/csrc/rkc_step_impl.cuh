@@ -231,6 +231,33 @@ __device__ __forceinline__ uint32_t cl_mode(uint32_t c) { return (S.cl[c][0] >> 
 __device__ __forceinline__ uint32_t cl_obj(uint32_t c) { return (S.cl[c][0] >> 16) & 0xFFu; }
 enum : uint32_t { CF_W0 = 0, CF_F = 1, CF_R = 2, CF_D = 3, CF_DEC = 4, CF_PC = 5 };
 
+// 16-B store with an L2 evict_last cache policy
+__device__ __forceinline__ void st_evict_last(uint4* p, const uint4 v) {
+  asm volatile(
+      "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+      "st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, pol;\n\t}" ::"l"(p),
+      "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+      : "memory");
+}
+// 16-B load / 4-B store with an L2 evict_last cache policy (lines reused by the next kernel)
+__device__ __forceinline__ uint4 ld_evict_last(const uint4* p) {
+  uint4 v;
+  asm volatile(
+      "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+      "ld.global.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], pol;\n\t}"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st32_evict_last(uint32_t* p, uint32_t v) {
+  asm volatile(
+      "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+      "st.global.L2::cache_hint.u32 [%0], %1, pol;\n\t}" ::"l"(p), "r"(v)
+      : "memory");
+}
+#ifndef RKC_HDR_EVICT_LAST
+#define RKC_HDR_EVICT_LAST 0   // hot headers kept in L2 between the step kernel and the next light pass
+#endif
 // ------------------------------ telemetry ----------------------------------
 __device__ __forceinline__ void write_event(uint32_t idx, uint32_t type, uint32_t seq,
                                             uint32_t slot, uint32_t reason, uint32_t mask,
@@ -2080,7 +2107,11 @@ __device__ __noinline__ void finish() {
     __syncwarp();
   }
   if (S.flags & F_HDR) {
+#if RKC_HDR_EVICT_LAST
+    if (lane_id() < H_HOT) st32_evict_last(S.hdrp + lane_id(), S.h[lane_id()]);
+#else
     if (lane_id() < H_HOT) S.hdrp[lane_id()] = S.h[lane_id()];
+#endif
   }
   __syncwarp();
   const uint32_t d = S.ctr[lane_id()];
@@ -2110,6 +2141,15 @@ __device__ __forceinline__ uint32_t bucket_of(uint32_t kind) {
   }
 }
 
+#ifndef RKC_LIGHT_ILP
+#define RKC_LIGHT_ILP 1   // traces per light-pass thread (loads of all of them in flight together)
+#endif
+#ifndef RKC_RQ_EVICT_LAST
+#define RKC_RQ_EVICT_LAST 0
+#endif
+#ifndef RKC_TICKET_EVICT_LAST
+#define RKC_TICKET_EVICT_LAST 1   // round 2: c5 -1.1 %
+#endif
 // K0: light pass, one thread per trace.  Completes the ops that provably
 // change nothing but a request record and a counter -- a NOP with no expiry
 // due, an ADVANCE that needs no new block (decode within the last block, or a
@@ -2125,6 +2165,221 @@ constexpr uint32_t kLightThreads = RKC_LIGHT_THREADS;
 
 // heavy-trace ticket: op (4 words), hot header words 0..11 (word 10 <- the trace id)
 constexpr uint32_t kTicketWords = 16u;
+#if RKC_LIGHT_ILP > 1
+// K0 with RKC_LIGHT_ILP traces per thread: every trace's op + header loads,
+// then every trace's request load, are issued before any is consumed, and one
+// pair of CTA barriers (bucket ranks) serves all of them.
+__global__ void __launch_bounds__(kLightThreads, RKC_LIGHT_MIN_CTAS) rkc_light_kernel(const __grid_constant__ StepArgs args) {
+  constexpr uint32_t LQ = RKC_LIGHT_ILP;
+  const PoolDev& p = args.p;
+  const uint32_t step = args.step;
+  uint32_t* cnt = p.bcnt + (step & 1u) * 8 * kBcntStride;
+  pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x < 8) p.bcnt[(((step + 1u) & 1u) * 8 + threadIdx.x) * kBcntStride] = 0;
+  const uint32_t lane = threadIdx.x & 31u;
+  __shared__ uint32_t s_cnt[8], s_base[8];
+  if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+  const bool small = p.NS <= 1024;  // one bitmap word per lane
+  uint32_t tq[LQ], kindq[LQ];
+  bool validq[LQ], heavyq[LQ], faq[LQ];
+  uint32_t fa_needq[LQ], fa_liveq[LQ], fa_ownerq[LQ];
+  uint4 opwq[LQ], hv0q[LQ], hv1q[LQ], hv2q[LQ], r0q[LQ], r1q[LQ];
+  // level 1: ops and hot headers of every trace of the thread
+#pragma unroll
+  for (uint32_t q = 0; q < LQ; ++q) {
+    tq[q] = (blockIdx.x * LQ + q) * kLightThreads + threadIdx.x;
+    validq[q] = tq[q] < p.num_traces;
+    opwq[q] = hv0q[q] = hv1q[q] = hv2q[q] = make_uint4(0, 0, 0, 0);
+    if (validq[q]) {
+      opwq[q] = __ldcs(args.ops + tq[q]);
+      const uint4* h4 = reinterpret_cast<const uint4*>(p.hdr + (size_t)tq[q] * H_NWORDS);
+      hv0q[q] = __ldcg(h4);
+      hv1q[q] = __ldcg(h4 + 1);
+      hv2q[q] = __ldcg(h4 + 2);
+    }
+  }
+  // level 2: the request record an ADVANCE / ADMIT decides on
+#pragma unroll
+  for (uint32_t q = 0; q < LQ; ++q) {
+    r0q[q] = r1q[q] = make_uint4(0, 0, 0, 0);
+    const uint32_t kind = opwq[q].x & 0xFFu, a = (opwq[q].x >> 8) & 0xFFu;
+    if (validq[q] && (kind == OP_ADVANCE || kind == OP_ADMIT) && a < p.Q) {
+      const uint4* rq4 = reinterpret_cast<const uint4*>(p.req + ((size_t)tq[q] * p.Q + a) * 8);
+      r0q[q] = __ldcg(rq4);
+      if (kind == OP_ADVANCE) r1q[q] = __ldcg(rq4 + 1);
+    }
+  }
+#pragma unroll
+  for (uint32_t q = 0; q < LQ; ++q) {
+    const uint32_t t = tq[q];
+    const uint4 opw = opwq[q], hv0 = hv0q[q], hv1 = hv1q[q], hv2 = hv2q[q];
+    bool heavy = false, fa = false;
+    uint32_t fa_need = 0, fa_live = 0, fa_owner = 0;
+    const uint32_t kind = opw.x & 0xFFu;
+    if (validq[q]) {
+      const uint32_t nexp = hv2.x;
+      const uint32_t a = (opw.x >> 8) & 0xFFu;
+      heavy = true;
+      if (kind == OP_NOP) {
+        heavy = step >= nexp;
+      } else if (kind == OP_ADVANCE && a < p.Q) {
+        uint32_t* rq = p.req + ((size_t)t * p.Q + a) * 8;
+        const uint4 r0 = r0q[q], r1 = r1q[q];
+        const uint32_t status = r0.x & 0xFFu, prompt = r0.y, chunk = r0.z, decode = r0.w;
+        const uint32_t done = r1.x, live = r1.y, held = r1.y + r1.z;  // own + shared hit blocks
+        if (step < nexp && status == R_RUNNING && (uint64_t)done < (uint64_t)prompt + decode) {
+          const uint32_t n = done < prompt ? min(chunk, prompt - done) : 1u;
+          const uint64_t need_total = ((uint64_t)done + n + kBlockTokens - 1) / kBlockTokens;
+          if (need_total <= held) {
+            rq[RQ_DONE] = done + n;
+            atomicAdd(p.ctr + (size_t)t * K_NCTR + K_OPS, 1u);
+            heavy = false;
+          } else if (small) {
+            const uint32_t need = (uint32_t)(need_total - held);
+            if ((uint64_t)hv1.z + hv1.y + need <= hv0.x && need <= hv1.x) {
+              fa = true;
+              fa_need = need;
+              fa_live = live;
+              fa_owner = a;
+              uint32_t* hw = p.hdr + (size_t)t * H_NWORDS;
+              hw[H_FREE] = hv1.x - need;
+              hw[H_ALIVE] = hv1.y + need;
+              rq[RQ_LIVE] = live + need;
+              rq[RQ_DONE] = done + n;
+              atomicAdd(p.ctr + (size_t)t * K_NCTR + K_OPS, 1u);
+              atomicAdd(p.ctr + (size_t)t * K_NCTR + K_BLOCKS_ALLOCATED, need);
+              atomicAdd(p.ctr + (size_t)t * K_NCTR + K_ALLOCATIONS, 1u);
+              heavy = false;
+            }
+          }
+        }
+      } else if (kind == OP_ADMIT && a < p.Q && ((opw.x >> 16) & 0xFFu) < p.O && (opw.x >> 24) <= 1 &&
+                 opw.y >= 1 && opw.z >= 1 && opw.y <= kMaxTokens && opw.w <= kMaxTokens) {
+        uint32_t* rq = p.req + ((size_t)t * p.Q + a) * 8;
+        const uint32_t status = r0q[q].x & 0xFFu;
+        if (step < nexp && status != R_RUNNING && status != R_DEFERRED) {
+          const uint64_t peak = ((uint64_t)opw.y + opw.w + kBlockTokens - 1) / kBlockTokens;
+          const uint32_t chk = (hv0.y >> 8) & 0xFFu;  // RESERVE admissions take the warp path
+          if (chk == ADMIT_NONE || (chk == ADMIT_PEAK && (uint64_t)hv1.z + hv1.y + peak <= hv0.x)) {
+            reinterpret_cast<uint4*>(rq)[0] =
+                make_uint4(R_RUNNING | ((opw.x >> 24) << 8) | (((opw.x >> 16) & 0xFFu) << 16), opw.y,
+                           opw.z, opw.w);
+            reinterpret_cast<uint4*>(rq)[1] = make_uint4(0, 0, 0, 0);  // done, live, hit
+            atomicAdd(p.ctr + (size_t)t * K_NCTR + K_OPS, 1u);
+            atomicAdd(p.ctr + (size_t)t * K_NCTR + K_ADMITTED, 1u);
+            heavy = false;
+          }
+        }
+      }
+    }
+    kindq[q] = kind; heavyq[q] = heavy; faq[q] = fa;
+    fa_needq[q] = fa_need; fa_liveq[q] = fa_live; fa_ownerq[q] = fa_owner;
+  }
+#pragma unroll 1
+  for (uint32_t q = 0; q < LQ; ++q) {
+    const uint32_t t = tq[q];
+    const bool fa = faq[q];
+    const uint32_t fa_need = fa_needq[q], fa_live = fa_liveq[q], fa_owner = fa_ownerq[q];
+    // free-only allocations, one trace at a time across the warp (lane = free
+    // bitmap word): the `need` lowest-id free blocks, positions live.. in
+    // block-id order (G24)
+    // (the bitmap words of up to 8 traces are loaded before any is consumed)
+    for (uint32_t fm = __ballot_sync(kFull, fa); fm;) {
+      uint32_t words[8], srcs[8], nb = 0;
+#pragma unroll
+      for (uint32_t q = 0; q < 8; ++q) {
+        srcs[q] = fm ? __ffs(fm) - 1 : 0u;
+        words[q] = 0;
+        if (fm) {
+          const uint32_t tq = __shfl_sync(kFull, t, srcs[q]);
+          if (lane < p.NS / 32) words[q] = __ldcg(p.fbm + (size_t)tq * (p.NS / 32) + lane);
+          fm &= fm - 1;
+          nb = q + 1;
+        }
+      }
+#pragma unroll
+      for (uint32_t q = 0; q < 8; ++q) {
+      if (q >= nb) break;
+      const uint32_t src = srcs[q];
+      const uint32_t tt = __shfl_sync(kFull, t, src), need = __shfl_sync(kFull, fa_need, src);
+      const uint32_t live = __shfl_sync(kFull, fa_live, src), owner = __shfl_sync(kFull, fa_owner, src);
+      uint32_t* fbm = p.fbm + (size_t)tt * (p.NS / 32);
+      const uint32_t word = words[q];
+      const uint32_t c = __popc(word);
+      const uint32_t incl = warp_incl_scan(c, lane);
+      const uint32_t before = incl - c;
+      const uint32_t take = before >= need ? 0u : min(c, need - before);
+      if (take > 0) {
+        const uint32_t tw = take == c ? word : word & ((1u << nth_set_bit(word, take + 1)) - 1u);
+        fbm[lane] = word & ~tw;
+      }
+#if RKC_LIGHT_RANKED
+      // rank-parallel: rank r (block at position live + r) goes to lane r % 32;
+      // its bitmap word is the first whose inclusive count exceeds r (the taken
+      // blocks of one allocation are usually a run inside one or two words)
+      uint32_t* key = p.key + (size_t)tt * p.NS;
+      uint32_t* meta = p.meta + (size_t)tt * p.NS;
+      for (uint32_t r0 = 0; r0 < need; r0 += 32) {
+        const uint32_t r = r0 + lane;
+        uint32_t sl = 0;
+#pragma unroll
+        for (uint32_t b = 16; b >= 1; b >>= 1)
+          if (__shfl_sync(kFull, incl, sl + b - 1) <= r) sl += b;
+        const uint32_t ws = __shfl_sync(kFull, word, sl & 31u), bs = __shfl_sync(kFull, before, sl & 31u);
+        if (r < need) {
+          const uint32_t b = sl * 32 + nth_set_bit(ws, r - bs + 1);
+          meta[b] = meta_make(kResActive, owner, live + r);
+          key[b] = kKeyActive;
+        }
+      }
+#else
+      if (take > 0) {
+        uint32_t tw = take == c ? word : word & ((1u << nth_set_bit(word, take + 1)) - 1u);
+        uint32_t* key = p.key + (size_t)tt * p.NS;
+        uint32_t* meta = p.meta + (size_t)tt * p.NS;
+        for (uint32_t r = live + before; tw; tw &= tw - 1, ++r) {
+          const uint32_t b = lane * 32 + __ffs(tw) - 1;
+          meta[b] = meta_make(kResActive, owner, r);
+          key[b] = kKeyActive;
+        }
+      }
+#endif
+      }
+    }
+  }
+  // bucket ranks of every trace of the thread, then one pair of CTA barriers
+  uint32_t offq[LQ], bkq[LQ], grpq[LQ];
+  __syncthreads();  // s_cnt initialised
+#pragma unroll
+  for (uint32_t q = 0; q < LQ; ++q) {
+    const bool heavy = heavyq[q];
+    const uint32_t bk = heavy ? bucket_of(kindq[q]) : 8u;
+    const uint32_t grp = __match_any_sync(kFull, bk);
+    const uint32_t leader = __ffs(grp) - 1;
+    uint32_t off = 0;
+    if (lane == leader && heavy) off = atomicAdd(&s_cnt[bk], __popc(grp));
+    offq[q] = __shfl_sync(kFull, off, leader) + __popc(grp & lanemask_lt());
+    bkq[q] = bk; grpq[q] = grp;
+  }
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    const uint32_t c = s_cnt[threadIdx.x];
+    s_base[threadIdx.x] = c ? atomicAdd(cnt + threadIdx.x * kBcntStride, c) : 0u;
+  }
+  __syncthreads();
+#pragma unroll
+  for (uint32_t q = 0; q < LQ; ++q) {
+    if (!heavyq[q]) continue;
+    const uint32_t bk = bkq[q];
+    uint4* tk = reinterpret_cast<uint4*>(p.perm) +
+                (kTicketWords / 4) * ((size_t)bk * p.num_traces + s_base[bk] + offq[q]);
+    tk[0] = opwq[q];
+    tk[1] = hv0q[q];
+    tk[2] = hv1q[q];
+    tk[3] = make_uint4(hv2q[q].x, hv2q[q].y, tq[q], 0u);
+  }
+}
+#else
 __global__ void __launch_bounds__(kLightThreads, RKC_LIGHT_MIN_CTAS) rkc_light_kernel(const __grid_constant__ StepArgs args) {
   const PoolDev& p = args.p;
   const uint32_t step = args.step;
@@ -2146,9 +2401,15 @@ __global__ void __launch_bounds__(kLightThreads, RKC_LIGHT_MIN_CTAS) rkc_light_k
       // level 1: the op and the trace's hot header (independent of the op)
       opw = __ldcs(args.ops + t);
       const uint32_t* h = p.hdr + (size_t)t * H_NWORDS;
+#if RKC_HDR_EVICT_LAST
+      hv0 = ld_evict_last(reinterpret_cast<const uint4*>(h));
+      hv1 = ld_evict_last(reinterpret_cast<const uint4*>(h) + 1);
+      hv2 = ld_evict_last(reinterpret_cast<const uint4*>(h) + 2);
+#else
       hv0 = __ldcg(reinterpret_cast<const uint4*>(h));      // U, policy, accept, seq
       hv1 = __ldcg(reinterpret_cast<const uint4*>(h) + 1);  // free, alive, P, mask
       hv2 = __ldcg(reinterpret_cast<const uint4*>(h) + 2);  // next expiry, event count
+#endif
       const uint32_t nexp = hv2.x;
       kind = opw.x & 0xFFu;
       const uint32_t a = (opw.x >> 8) & 0xFFu;
@@ -2302,13 +2563,31 @@ __global__ void __launch_bounds__(kLightThreads, RKC_LIGHT_MIN_CTAS) rkc_light_k
     if (heavy) {  // the ticket: op, header words 0..11 (word 10 <- the trace id)[, request]
       uint4* tk = reinterpret_cast<uint4*>(p.perm) +
                   (kTicketWords / 4) * ((size_t)bk * p.num_traces + cbase + off + __popc(grp & lanemask_lt()));
+#if RKC_RQ_EVICT_LAST
+      {  // the request record the step kernel loads first: pinned in L2 the same way
+        const uint32_t a = (opw.x >> 8) & 0xFFu;
+        if ((kind == OP_ADVANCE || kind == OP_COMPLETE || kind == OP_ADMIT || kind == OP_HIT_ADMIT) && a < p.Q)
+          asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p.req + ((size_t)t * p.Q + a) * 8));
+      }
+#endif
+#if RKC_TICKET_EVICT_LAST
+      // tickets are read back by the step kernel right after this pass: keep
+      // them in L2 ahead of the streamed op / header / request lines
+      st_evict_last(tk + 0, opw);
+      st_evict_last(tk + 1, hv0);
+      st_evict_last(tk + 2, hv1);
+      st_evict_last(tk + 3, make_uint4(hv2.x, hv2.y, t, 0u));
+#else
       tk[0] = opw;
       tk[1] = hv0;
       tk[2] = hv1;
       tk[3] = make_uint4(hv2.x, hv2.y, t, 0u);
+#endif
     }
   }
 }
+
+#endif  // RKC_LIGHT_ILP
 
 // bucketed item i of this step -> its trace (false past the heavy count)
 __device__ __forceinline__ bool item_trace(const StepArgs& args, uint32_t i, const uint32_t*& tk) {
@@ -2560,7 +2839,7 @@ static cudaError_t launch_pdl(Kernel kernel, uint32_t grid, uint32_t block, cuda
 // host launcher: one launch = one lockstep step over all traces
 cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, cudaStream_t st) {
   StepArgs args{p, reinterpret_cast<const uint4*>(ops_step), step};
-  const uint32_t lct = (p.num_traces + kLightThreads - 1) / kLightThreads;
+  const uint32_t lct = (p.num_traces + kLightThreads * RKC_LIGHT_ILP - 1) / (kLightThreads * RKC_LIGHT_ILP);
 // one light thread per trace (round 2: the former cap of 16 CTAs per SM, i.e. 3.3 traces per
 // thread at c5, measured 1 % slower per lockstep step: profiles/r02/experiments.md)
 #ifndef RKC_LIGHT_MAX_CTAS

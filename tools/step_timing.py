@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--nop", action="store_true", help="all-NOP op stream (launch floor)")
     ap.add_argument("--tag", default="")
+    ap.add_argument("--per-step", action="store_true", help="time every lockstep step separately")
     a = ap.parse_args()
     import torch
     from paper_2605_24259_b200 import gen, rkc
@@ -44,6 +45,19 @@ def main():
         if r:
             ts.append(e0.elapsed_time(e1))
     ms = float(np.median(ts))
+    if a.per_step:  # one more replay, one rkc_step_batch call and one event pair per step
+        pool.rkc_pool_reset()
+        torch.cuda.synchronize()
+        row = a.traces * 16
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
+        evs[0].record()
+        for st in range(a.steps):
+            pool.rkc_step_batch(d[st * row:(st + 1) * row], 1)
+            evs[st + 1].record()
+        torch.cuda.synchronize()
+        us = [1000 * evs[i].elapsed_time(evs[i + 1]) for i in range(a.steps)]
+        print(f"{a.tag:16s} per-step us: " + " ".join(f"{i}:{us[i]:.0f}" for i in range(0, a.steps, 16)) +
+              f"  sum {sum(us) / 1000:.2f} ms")
     ctr = torch.zeros(a.traces * 32, dtype=torch.int32, device="cuda")
     pool.rkc_telemetry_read(counters_out=ctr)
     w = torch.arange(1, a.traces * 32 + 1, device="cuda", dtype=torch.int64) % 1000003
