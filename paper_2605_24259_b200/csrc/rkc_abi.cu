@@ -299,7 +299,7 @@ rkc_status run_init(rkc_pool* p, cudaStream_t st) {
   CUDA_TRY(cudaMemsetAsync(p->d.req, 0, (size_t)p->d.num_traces * p->d.Q * 32, st));
   CUDA_TRY(cudaMemsetAsync(p->d.ctr, 0, (size_t)p->d.num_traces * K_NCTR * 4, st));
   CUDA_TRY(cudaMemsetAsync(p->staged, 0, sizeof(uint4) * p->d.num_traces, st));
-  CUDA_TRY(cudaMemsetAsync(p->d.bcnt, 0, 16 * 32 * 4, st));  // room for 128-B spaced counters
+  CUDA_TRY(cudaMemsetAsync(p->d.bcnt, 0, 16 * 4, st));
   CUDA_TRY(cudaMemsetAsync(p->owner_tag, 0xFF, sizeof(uint32_t) * p->d.num_traces, st));
   CUDA_TRY(cudaGetLastError());
   p->step = 0;
@@ -456,7 +456,7 @@ rkc_status rkc_pool_create(const rkc_pool_config* config, const rkc_trace_config
   ALLOC(d.ctr, T * K_NCTR * 4);
   ALLOC(d.ev, T * (size_t)d.EPT * 32);
   ALLOC(d.perm, T * 8 * 64);   // 64-B tickets (rkc_step_impl.cuh kTicketWords)
-  ALLOC(d.bcnt, 16 * 32 * 4);
+  ALLOC(d.bcnt, 16 * 4);
   ALLOC(p->tcfg, T * 12);
   ALLOC(p->staged, T * 16);
   ALLOC(p->owner_tag, T * 4);

@@ -61,46 +61,8 @@ constexpr int kCrewUnroll = RKC_CREW_UNROLL;  // block vectors in flight per lan
 #endif
 constexpr uint32_t kObjMax = RKC_OMAX;
 
-#ifndef RKC_ITEMS_PER_CTA
-#define RKC_ITEMS_PER_CTA 1   // small pools: heavy items per one-warp CTA (1 or 2)
-#endif
-#ifndef RKC_RUN_ITEM_ATTR
-#if RKC_ITEMS_PER_CTA == 2
-#define RKC_RUN_ITEM_ATTR __noinline__   // one call per item (an inlined loop body spills)
-#else
-#define RKC_RUN_ITEM_ATTR __forceinline__
-#endif
-#endif
-#ifndef RKC_BCNT_STRIDE
-#define RKC_BCNT_STRIDE 1   // words between the bucket counters (32: one 128-B line each)
-#endif
-constexpr uint32_t kBcntStride = RKC_BCNT_STRIDE;
-#ifndef RKC_CREW_VEC
-#define RKC_CREW_VEC 1   // crew apply / touch: one 16-B read-back per vector instead of one load per block (c4 -10 %)
-#endif
-#ifndef RKC_BIG_PRELOAD
-#define RKC_BIG_PRELOAD 0
-#endif
-#ifndef RKC_SEARCH_F32
-#define RKC_SEARCH_F32 1   // threshold-search probe estimates in fp32 instead of 64-bit integer division
-#endif
-#ifndef RKC_CTR_RED
-#define RKC_CTR_RED 0
-#endif
-#ifndef RKC_TICKET_UNIFORM
-#define RKC_TICKET_UNIFORM 1   // ticket fields as uniform loads instead of per-lane words + shuffles
-#endif
-#ifndef RKC_TICKET_REVERSE
-#define RKC_TICKET_REVERSE 0   // items of a bucket in reverse ticket order (latest light-pass traces first)
-#endif
-#ifndef RKC_LIGHT_WARP_ATOMICS
-#define RKC_LIGHT_WARP_ATOMICS 0
-#endif
 #ifndef RKC_LIGHT_RANKED
 #define RKC_LIGHT_RANKED 1   // free-only takes: one rank per lane instead of a bit loop per word
-#endif
-#ifndef RKC_FREE_RANKED
-#define RKC_FREE_RANKED 0    // the same in the step kernel's free-only allocation
 #endif
 #ifndef RKC_LIGHT_MIN_CTAS
 #define RKC_LIGHT_MIN_CTAS 10   // 48 registers: 10 light CTAs per SM
@@ -215,14 +177,7 @@ __device__ __forceinline__ void flag_set(uint32_t f) {
 }
 __device__ __forceinline__ uint32_t lowering() { return S.h[H_POLICY] & 0xFFu; }
 __device__ __forceinline__ void ctr_add(uint32_t k, uint32_t v) {
-#if RKC_CTR_RED
-  // lane 0's predicated shared-memory reduction: no load / use round trip
-  // (read back only in finish(), after a __syncwarp)
-  asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %0, 0;\n\t@p red.shared.add.u32 [%1], %2;\n\t}"
-               ::"r"(lane_id()), "r"((uint32_t)__cvta_generic_to_shared(&S.ctr[k])), "r"(v) : "memory");
-#else
   if (lane_id() == 0) S.ctr[k] += v;
-#endif
 }
 
 // claim record accessors (slot c)
@@ -239,25 +194,6 @@ __device__ __forceinline__ void st_evict_last(uint4* p, const uint4 v) {
       "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
       : "memory");
 }
-// 16-B load / 4-B store with an L2 evict_last cache policy (lines reused by the next kernel)
-__device__ __forceinline__ uint4 ld_evict_last(const uint4* p) {
-  uint4 v;
-  asm volatile(
-      "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
-      "ld.global.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], pol;\n\t}"
-      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-      : "l"(p));
-  return v;
-}
-__device__ __forceinline__ void st32_evict_last(uint32_t* p, uint32_t v) {
-  asm volatile(
-      "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
-      "st.global.L2::cache_hint.u32 [%0], %1, pol;\n\t}" ::"l"(p), "r"(v)
-      : "memory");
-}
-#ifndef RKC_HDR_EVICT_LAST
-#define RKC_HDR_EVICT_LAST 0   // hot headers kept in L2 between the step kernel and the next light pass
-#endif
 // ------------------------------ telemetry ----------------------------------
 __device__ __forceinline__ void write_event(uint32_t idx, uint32_t type, uint32_t seq,
                                             uint32_t slot, uint32_t reason, uint32_t mask,
@@ -540,23 +476,17 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
         const uint32_t cnt = __popc(tb);
         const uint32_t Sc = warp_incl_scan(cnt, lane);
         uint32_t r = rank + Sc - cnt;
-#if RKC_CREW_VEC
         // the vector's meta words in one 16-B load (not one dependent load per victim)
         const bool anyv = (tb & 1u && v.x >= kC1) || (tb & 2u && v.y >= kC1) || (tb & 4u && v.z >= kC1) ||
                           (tb & 8u && v.w >= kC1);
         const uint4 mvv = anyv ? __ldcg(meta4 + j * 32 + lane) : make_uint4(0, 0, 0, 0);
-#endif
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           if (!((tb >> e) & 1u)) continue;
           const uint32_t bb = block_of(j, e);
           const uint32_t pos = base + r++;
           if (el(v, e) >= kC1) {  // a victim: attributed by its object's claim now (Table 4)
-#if RKC_CREW_VEC
             const uint32_t m = el(mvv, e);
-#else
-            const uint32_t m = __ldcg(meta + bb);
-#endif
             const uint32_t o = meta_owner(m);
             const uint32_t cc = obj_claim(S.obj0[o]);
             const uint32_t st = cc < 32 ? cl_state(cc) : C_EMPTY;
@@ -646,7 +576,6 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
       for (uint32_t j = j0; j < j1; ++j) {
         crew_pf(meta4, j, j1);
         const uint4 mv = __ldcg(meta4 + j * 32 + lane);
-#if RKC_CREW_VEC
         // matching blocks: the key vector read back in one 16-B load
         uint32_t hit = 0;
 #pragma unroll
@@ -661,16 +590,6 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
             if ((hit >> e) & 1u)
               key[block_of(j, e)] = (el(kv, e) & ~kSeqMask) | (seq_base + (L - 1 - meta_pos(el(mv, e))));
         }
-#else
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint32_t m = el(mv, e);
-          if (meta_res(m) == kResCached && meta_owner(m) == ob && meta_pos(m) < L) {
-            const uint32_t bb = block_of(j, e);
-            key[bb] = (__ldcg(key + bb) & ~kSeqMask) | (seq_base + (L - 1 - meta_pos(m)));
-          }
-        }
-#endif
       }
       break;
     }
@@ -1241,35 +1160,7 @@ __device__ __noinline__ void alloc_free(uint32_t k, uint32_t owner, bool insert,
     const uint32_t Sc = warp_incl_scan(c, lane_id());
     const uint32_t before = acc + Sc - c;
     const uint32_t take = before >= k ? 0u : min(c, k - before);
-#if RKC_FREE_RANKED
-    // rank-parallel (as in the light pass): rank r of this chunk -> lane r % 32
-    if (take > 0) fbm[wi] = word & ~(take == c ? word : word & ((1u << nth_set_bit(word, take + 1)) - 1u));
-    const uint32_t tot = __shfl_sync(kFull, Sc, 31);
-    const uint32_t ntake = min(tot, k - acc);
-    for (uint32_t r0 = 0; r0 < ntake; r0 += 32) {
-      const uint32_t rr = r0 + lane_id();
-      uint32_t sl = 0;
-#pragma unroll
-      for (uint32_t b = 16; b >= 1; b >>= 1)
-        if (__shfl_sync(kFull, Sc, sl + b - 1) <= rr) sl += b;
-      const uint32_t ws = __shfl_sync(kFull, word, sl), bs = __shfl_sync(kFull, Sc - c, sl);
-      if (rr < ntake) {
-        const uint32_t bb = (w0 + sl) * 32 + nth_set_bit(ws, rr - bs + 1);
-        const uint32_t pos = base + acc + rr;
-        if (insert) {
-          const uint32_t cls = pos < l3 ? 3u : (pos < l2 ? 2u : 1u);
-          key[bb] = (cls << kClassShift) | (seq_base + (k - 1 - pos));
-          meta[bb] = meta_make(kResCached, owner, pos);
-        } else {
-          key[bb] = kKeyActive;
-          meta[bb] = meta_make(kResActive, owner, pos);
-        }
-      }
-    }
-    if (false) {
-#else
     if (take > 0) {
-#endif
       uint32_t tw = take == c ? word : word & ((1u << nth_set_bit(word, take + 1)) - 1u);
       fbm[wi] = word & ~tw;
       uint32_t r = before;
@@ -1399,14 +1290,10 @@ __device__ RKC_EVICT_ATTR void alloc_evict(uint32_t k, uint32_t owner, bool inse
     if (!bracket) {
       if (!staged && it > 0 && clo > clo0) {
         // secant step, but never less than twice the last step (no creeping)
-#if RKC_SEARCH_F32
         // fp32 estimate (the probe position only steers the search; the
         // taken set {key <= T} is the same for any probe sequence)
         const float df = fminf((float)(k - clo) * (float)(lo - lo0) * 1.25f / (float)(clo - clo0), 4.0e9f);
         uint64_t d = (uint64_t)__float2uint_rz(df) + 1;
-#else
-        uint64_t d = ((uint64_t)(k - clo) * (lo - lo0) * 5) / ((uint64_t)(clo - clo0) * 4) + 1;
-#endif
         d = max(d, 2 * (uint64_t)last_d);
         last_d = (uint32_t)min(d, (uint64_t)0xFFFFFFFFu);
         m = (uint32_t)min((uint64_t)lo + d, (uint64_t)top);
@@ -1419,12 +1306,8 @@ __device__ RKC_EVICT_ATTR void alloc_evict(uint32_t k, uint32_t owner, bool inse
     } else {
       const uint32_t span = hi - lo;
       const bool interp = staged ? (it & 1u) != 0 : (bi++ & 1u) == 0;
-#if RKC_SEARCH_F32
       m = interp ? lo + __float2uint_rz(fminf((float)(k - clo) * (float)span / (float)(chi - clo), (float)span))
                  : lo + span / 2;
-#else
-      m = interp ? lo + (uint32_t)(((uint64_t)(k - clo) * span) / (chi - clo)) : lo + span / 2;
-#endif
       m = max(m, lo + 1);
       m = min(m, hi - 1);
     }
@@ -2107,11 +1990,7 @@ __device__ __noinline__ void finish() {
     __syncwarp();
   }
   if (S.flags & F_HDR) {
-#if RKC_HDR_EVICT_LAST
-    if (lane_id() < H_HOT) st32_evict_last(S.hdrp + lane_id(), S.h[lane_id()]);
-#else
     if (lane_id() < H_HOT) S.hdrp[lane_id()] = S.h[lane_id()];
-#endif
   }
   __syncwarp();
   const uint32_t d = S.ctr[lane_id()];
@@ -2141,15 +2020,6 @@ __device__ __forceinline__ uint32_t bucket_of(uint32_t kind) {
   }
 }
 
-#ifndef RKC_LIGHT_ILP
-#define RKC_LIGHT_ILP 1   // traces per light-pass thread (loads of all of them in flight together)
-#endif
-#ifndef RKC_RQ_EVICT_LAST
-#define RKC_RQ_EVICT_LAST 0
-#endif
-#ifndef RKC_TICKET_EVICT_LAST
-#define RKC_TICKET_EVICT_LAST 1   // round 2: c5 -1.1 %
-#endif
 // K0: light pass, one thread per trace.  Completes the ops that provably
 // change nothing but a request record and a counter -- a NOP with no expiry
 // due, an ADVANCE that needs no new block (decode within the last block, or a
@@ -2165,227 +2035,12 @@ constexpr uint32_t kLightThreads = RKC_LIGHT_THREADS;
 
 // heavy-trace ticket: op (4 words), hot header words 0..11 (word 10 <- the trace id)
 constexpr uint32_t kTicketWords = 16u;
-#if RKC_LIGHT_ILP > 1
-// K0 with RKC_LIGHT_ILP traces per thread: every trace's op + header loads,
-// then every trace's request load, are issued before any is consumed, and one
-// pair of CTA barriers (bucket ranks) serves all of them.
-__global__ void __launch_bounds__(kLightThreads, RKC_LIGHT_MIN_CTAS) rkc_light_kernel(const __grid_constant__ StepArgs args) {
-  constexpr uint32_t LQ = RKC_LIGHT_ILP;
-  const PoolDev& p = args.p;
-  const uint32_t step = args.step;
-  uint32_t* cnt = p.bcnt + (step & 1u) * 8 * kBcntStride;
-  pdl_wait();
-  if (blockIdx.x == 0 && threadIdx.x < 8) p.bcnt[(((step + 1u) & 1u) * 8 + threadIdx.x) * kBcntStride] = 0;
-  const uint32_t lane = threadIdx.x & 31u;
-  __shared__ uint32_t s_cnt[8], s_base[8];
-  if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
-  const bool small = p.NS <= 1024;  // one bitmap word per lane
-  uint32_t tq[LQ], kindq[LQ];
-  bool validq[LQ], heavyq[LQ], faq[LQ];
-  uint32_t fa_needq[LQ], fa_liveq[LQ], fa_ownerq[LQ];
-  uint4 opwq[LQ], hv0q[LQ], hv1q[LQ], hv2q[LQ], r0q[LQ], r1q[LQ];
-  // level 1: ops and hot headers of every trace of the thread
-#pragma unroll
-  for (uint32_t q = 0; q < LQ; ++q) {
-    tq[q] = (blockIdx.x * LQ + q) * kLightThreads + threadIdx.x;
-    validq[q] = tq[q] < p.num_traces;
-    opwq[q] = hv0q[q] = hv1q[q] = hv2q[q] = make_uint4(0, 0, 0, 0);
-    if (validq[q]) {
-      opwq[q] = __ldcs(args.ops + tq[q]);
-      const uint4* h4 = reinterpret_cast<const uint4*>(p.hdr + (size_t)tq[q] * H_NWORDS);
-      hv0q[q] = __ldcg(h4);
-      hv1q[q] = __ldcg(h4 + 1);
-      hv2q[q] = __ldcg(h4 + 2);
-    }
-  }
-  // level 2: the request record an ADVANCE / ADMIT decides on
-#pragma unroll
-  for (uint32_t q = 0; q < LQ; ++q) {
-    r0q[q] = r1q[q] = make_uint4(0, 0, 0, 0);
-    const uint32_t kind = opwq[q].x & 0xFFu, a = (opwq[q].x >> 8) & 0xFFu;
-    if (validq[q] && (kind == OP_ADVANCE || kind == OP_ADMIT) && a < p.Q) {
-      const uint4* rq4 = reinterpret_cast<const uint4*>(p.req + ((size_t)tq[q] * p.Q + a) * 8);
-      r0q[q] = __ldcg(rq4);
-      if (kind == OP_ADVANCE) r1q[q] = __ldcg(rq4 + 1);
-    }
-  }
-#pragma unroll
-  for (uint32_t q = 0; q < LQ; ++q) {
-    const uint32_t t = tq[q];
-    const uint4 opw = opwq[q], hv0 = hv0q[q], hv1 = hv1q[q], hv2 = hv2q[q];
-    bool heavy = false, fa = false;
-    uint32_t fa_need = 0, fa_live = 0, fa_owner = 0;
-    const uint32_t kind = opw.x & 0xFFu;
-    if (validq[q]) {
-      const uint32_t nexp = hv2.x;
-      const uint32_t a = (opw.x >> 8) & 0xFFu;
-      heavy = true;
-      if (kind == OP_NOP) {
-        heavy = step >= nexp;
-      } else if (kind == OP_ADVANCE && a < p.Q) {
-        uint32_t* rq = p.req + ((size_t)t * p.Q + a) * 8;
-        const uint4 r0 = r0q[q], r1 = r1q[q];
-        const uint32_t status = r0.x & 0xFFu, prompt = r0.y, chunk = r0.z, decode = r0.w;
-        const uint32_t done = r1.x, live = r1.y, held = r1.y + r1.z;  // own + shared hit blocks
-        if (step < nexp && status == R_RUNNING && (uint64_t)done < (uint64_t)prompt + decode) {
-          const uint32_t n = done < prompt ? min(chunk, prompt - done) : 1u;
-          const uint64_t need_total = ((uint64_t)done + n + kBlockTokens - 1) / kBlockTokens;
-          if (need_total <= held) {
-            rq[RQ_DONE] = done + n;
-            atomicAdd(p.ctr + (size_t)t * K_NCTR + K_OPS, 1u);
-            heavy = false;
-          } else if (small) {
-            const uint32_t need = (uint32_t)(need_total - held);
-            if ((uint64_t)hv1.z + hv1.y + need <= hv0.x && need <= hv1.x) {
-              fa = true;
-              fa_need = need;
-              fa_live = live;
-              fa_owner = a;
-              uint32_t* hw = p.hdr + (size_t)t * H_NWORDS;
-              hw[H_FREE] = hv1.x - need;
-              hw[H_ALIVE] = hv1.y + need;
-              rq[RQ_LIVE] = live + need;
-              rq[RQ_DONE] = done + n;
-              atomicAdd(p.ctr + (size_t)t * K_NCTR + K_OPS, 1u);
-              atomicAdd(p.ctr + (size_t)t * K_NCTR + K_BLOCKS_ALLOCATED, need);
-              atomicAdd(p.ctr + (size_t)t * K_NCTR + K_ALLOCATIONS, 1u);
-              heavy = false;
-            }
-          }
-        }
-      } else if (kind == OP_ADMIT && a < p.Q && ((opw.x >> 16) & 0xFFu) < p.O && (opw.x >> 24) <= 1 &&
-                 opw.y >= 1 && opw.z >= 1 && opw.y <= kMaxTokens && opw.w <= kMaxTokens) {
-        uint32_t* rq = p.req + ((size_t)t * p.Q + a) * 8;
-        const uint32_t status = r0q[q].x & 0xFFu;
-        if (step < nexp && status != R_RUNNING && status != R_DEFERRED) {
-          const uint64_t peak = ((uint64_t)opw.y + opw.w + kBlockTokens - 1) / kBlockTokens;
-          const uint32_t chk = (hv0.y >> 8) & 0xFFu;  // RESERVE admissions take the warp path
-          if (chk == ADMIT_NONE || (chk == ADMIT_PEAK && (uint64_t)hv1.z + hv1.y + peak <= hv0.x)) {
-            reinterpret_cast<uint4*>(rq)[0] =
-                make_uint4(R_RUNNING | ((opw.x >> 24) << 8) | (((opw.x >> 16) & 0xFFu) << 16), opw.y,
-                           opw.z, opw.w);
-            reinterpret_cast<uint4*>(rq)[1] = make_uint4(0, 0, 0, 0);  // done, live, hit
-            atomicAdd(p.ctr + (size_t)t * K_NCTR + K_OPS, 1u);
-            atomicAdd(p.ctr + (size_t)t * K_NCTR + K_ADMITTED, 1u);
-            heavy = false;
-          }
-        }
-      }
-    }
-    kindq[q] = kind; heavyq[q] = heavy; faq[q] = fa;
-    fa_needq[q] = fa_need; fa_liveq[q] = fa_live; fa_ownerq[q] = fa_owner;
-  }
-#pragma unroll 1
-  for (uint32_t q = 0; q < LQ; ++q) {
-    const uint32_t t = tq[q];
-    const bool fa = faq[q];
-    const uint32_t fa_need = fa_needq[q], fa_live = fa_liveq[q], fa_owner = fa_ownerq[q];
-    // free-only allocations, one trace at a time across the warp (lane = free
-    // bitmap word): the `need` lowest-id free blocks, positions live.. in
-    // block-id order (G24)
-    // (the bitmap words of up to 8 traces are loaded before any is consumed)
-    for (uint32_t fm = __ballot_sync(kFull, fa); fm;) {
-      uint32_t words[8], srcs[8], nb = 0;
-#pragma unroll
-      for (uint32_t q = 0; q < 8; ++q) {
-        srcs[q] = fm ? __ffs(fm) - 1 : 0u;
-        words[q] = 0;
-        if (fm) {
-          const uint32_t tq = __shfl_sync(kFull, t, srcs[q]);
-          if (lane < p.NS / 32) words[q] = __ldcg(p.fbm + (size_t)tq * (p.NS / 32) + lane);
-          fm &= fm - 1;
-          nb = q + 1;
-        }
-      }
-#pragma unroll
-      for (uint32_t q = 0; q < 8; ++q) {
-      if (q >= nb) break;
-      const uint32_t src = srcs[q];
-      const uint32_t tt = __shfl_sync(kFull, t, src), need = __shfl_sync(kFull, fa_need, src);
-      const uint32_t live = __shfl_sync(kFull, fa_live, src), owner = __shfl_sync(kFull, fa_owner, src);
-      uint32_t* fbm = p.fbm + (size_t)tt * (p.NS / 32);
-      const uint32_t word = words[q];
-      const uint32_t c = __popc(word);
-      const uint32_t incl = warp_incl_scan(c, lane);
-      const uint32_t before = incl - c;
-      const uint32_t take = before >= need ? 0u : min(c, need - before);
-      if (take > 0) {
-        const uint32_t tw = take == c ? word : word & ((1u << nth_set_bit(word, take + 1)) - 1u);
-        fbm[lane] = word & ~tw;
-      }
-#if RKC_LIGHT_RANKED
-      // rank-parallel: rank r (block at position live + r) goes to lane r % 32;
-      // its bitmap word is the first whose inclusive count exceeds r (the taken
-      // blocks of one allocation are usually a run inside one or two words)
-      uint32_t* key = p.key + (size_t)tt * p.NS;
-      uint32_t* meta = p.meta + (size_t)tt * p.NS;
-      for (uint32_t r0 = 0; r0 < need; r0 += 32) {
-        const uint32_t r = r0 + lane;
-        uint32_t sl = 0;
-#pragma unroll
-        for (uint32_t b = 16; b >= 1; b >>= 1)
-          if (__shfl_sync(kFull, incl, sl + b - 1) <= r) sl += b;
-        const uint32_t ws = __shfl_sync(kFull, word, sl & 31u), bs = __shfl_sync(kFull, before, sl & 31u);
-        if (r < need) {
-          const uint32_t b = sl * 32 + nth_set_bit(ws, r - bs + 1);
-          meta[b] = meta_make(kResActive, owner, live + r);
-          key[b] = kKeyActive;
-        }
-      }
-#else
-      if (take > 0) {
-        uint32_t tw = take == c ? word : word & ((1u << nth_set_bit(word, take + 1)) - 1u);
-        uint32_t* key = p.key + (size_t)tt * p.NS;
-        uint32_t* meta = p.meta + (size_t)tt * p.NS;
-        for (uint32_t r = live + before; tw; tw &= tw - 1, ++r) {
-          const uint32_t b = lane * 32 + __ffs(tw) - 1;
-          meta[b] = meta_make(kResActive, owner, r);
-          key[b] = kKeyActive;
-        }
-      }
-#endif
-      }
-    }
-  }
-  // bucket ranks of every trace of the thread, then one pair of CTA barriers
-  uint32_t offq[LQ], bkq[LQ], grpq[LQ];
-  __syncthreads();  // s_cnt initialised
-#pragma unroll
-  for (uint32_t q = 0; q < LQ; ++q) {
-    const bool heavy = heavyq[q];
-    const uint32_t bk = heavy ? bucket_of(kindq[q]) : 8u;
-    const uint32_t grp = __match_any_sync(kFull, bk);
-    const uint32_t leader = __ffs(grp) - 1;
-    uint32_t off = 0;
-    if (lane == leader && heavy) off = atomicAdd(&s_cnt[bk], __popc(grp));
-    offq[q] = __shfl_sync(kFull, off, leader) + __popc(grp & lanemask_lt());
-    bkq[q] = bk; grpq[q] = grp;
-  }
-  __syncthreads();
-  if (threadIdx.x < 8) {
-    const uint32_t c = s_cnt[threadIdx.x];
-    s_base[threadIdx.x] = c ? atomicAdd(cnt + threadIdx.x * kBcntStride, c) : 0u;
-  }
-  __syncthreads();
-#pragma unroll
-  for (uint32_t q = 0; q < LQ; ++q) {
-    if (!heavyq[q]) continue;
-    const uint32_t bk = bkq[q];
-    uint4* tk = reinterpret_cast<uint4*>(p.perm) +
-                (kTicketWords / 4) * ((size_t)bk * p.num_traces + s_base[bk] + offq[q]);
-    tk[0] = opwq[q];
-    tk[1] = hv0q[q];
-    tk[2] = hv1q[q];
-    tk[3] = make_uint4(hv2q[q].x, hv2q[q].y, tq[q], 0u);
-  }
-}
-#else
 __global__ void __launch_bounds__(kLightThreads, RKC_LIGHT_MIN_CTAS) rkc_light_kernel(const __grid_constant__ StepArgs args) {
   const PoolDev& p = args.p;
   const uint32_t step = args.step;
-  uint32_t* cnt = p.bcnt + (step & 1u) * 8 * kBcntStride;
+  uint32_t* cnt = p.bcnt + (step & 1u) * 8;
   pdl_wait();
-  if (blockIdx.x == 0 && threadIdx.x < 8) p.bcnt[(((step + 1u) & 1u) * 8 + threadIdx.x) * kBcntStride] = 0;
+  if (blockIdx.x == 0 && threadIdx.x < 8) p.bcnt[(((step + 1u) & 1u) * 8 + threadIdx.x)] = 0;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t stride = gridDim.x * blockDim.x;
   __shared__ uint32_t s_cnt[8], s_base[8];
@@ -2401,15 +2056,9 @@ __global__ void __launch_bounds__(kLightThreads, RKC_LIGHT_MIN_CTAS) rkc_light_k
       // level 1: the op and the trace's hot header (independent of the op)
       opw = __ldcs(args.ops + t);
       const uint32_t* h = p.hdr + (size_t)t * H_NWORDS;
-#if RKC_HDR_EVICT_LAST
-      hv0 = ld_evict_last(reinterpret_cast<const uint4*>(h));
-      hv1 = ld_evict_last(reinterpret_cast<const uint4*>(h) + 1);
-      hv2 = ld_evict_last(reinterpret_cast<const uint4*>(h) + 2);
-#else
       hv0 = __ldcg(reinterpret_cast<const uint4*>(h));      // U, policy, accept, seq
       hv1 = __ldcg(reinterpret_cast<const uint4*>(h) + 1);  // free, alive, P, mask
       hv2 = __ldcg(reinterpret_cast<const uint4*>(h) + 2);  // next expiry, event count
-#endif
       const uint32_t nexp = hv2.x;
       kind = opw.x & 0xFFu;
       const uint32_t a = (opw.x >> 8) & 0xFFu;
@@ -2543,83 +2192,63 @@ __global__ void __launch_bounds__(kLightThreads, RKC_LIGHT_MIN_CTAS) rkc_light_k
     const uint32_t grp = __match_any_sync(kFull, bk);
     const uint32_t leader = __ffs(grp) - 1;
     uint32_t off = 0;
-#if RKC_LIGHT_WARP_ATOMICS
-    // one global atomic per (warp, bucket): no CTA barrier
-    if (lane == leader && heavy) off = atomicAdd(cnt + bk * kBcntStride, __popc(grp));
-    off = __shfl_sync(kFull, off, leader);
-    const uint32_t cbase = 0;
-#else
     if (lane == leader && heavy) off = atomicAdd(&s_cnt[bk], __popc(grp));
     off = __shfl_sync(kFull, off, leader);
     __syncthreads();
     if (threadIdx.x < 8) {
       const uint32_t c = s_cnt[threadIdx.x];
-      s_base[threadIdx.x] = c ? atomicAdd(cnt + threadIdx.x * kBcntStride, c) : 0u;
+      s_base[threadIdx.x] = c ? atomicAdd(cnt + threadIdx.x, c) : 0u;
       s_cnt[threadIdx.x] = 0;
     }
     __syncthreads();
     const uint32_t cbase = heavy ? s_base[bk] : 0u;
-#endif
     if (heavy) {  // the ticket: op, header words 0..11 (word 10 <- the trace id)[, request]
       uint4* tk = reinterpret_cast<uint4*>(p.perm) +
                   (kTicketWords / 4) * ((size_t)bk * p.num_traces + cbase + off + __popc(grp & lanemask_lt()));
-#if RKC_RQ_EVICT_LAST
-      {  // the request record the step kernel loads first: pinned in L2 the same way
-        const uint32_t a = (opw.x >> 8) & 0xFFu;
-        if ((kind == OP_ADVANCE || kind == OP_COMPLETE || kind == OP_ADMIT || kind == OP_HIT_ADMIT) && a < p.Q)
-          asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p.req + ((size_t)t * p.Q + a) * 8));
-      }
-#endif
-#if RKC_TICKET_EVICT_LAST
       // tickets are read back by the step kernel right after this pass: keep
       // them in L2 ahead of the streamed op / header / request lines
       st_evict_last(tk + 0, opw);
       st_evict_last(tk + 1, hv0);
       st_evict_last(tk + 2, hv1);
       st_evict_last(tk + 3, make_uint4(hv2.x, hv2.y, t, 0u));
-#else
-      tk[0] = opw;
-      tk[1] = hv0;
-      tk[2] = hv1;
-      tk[3] = make_uint4(hv2.x, hv2.y, t, 0u);
-#endif
     }
   }
 }
 
-#endif  // RKC_LIGHT_ILP
 
-// bucketed item i of this step -> its trace (false past the heavy count)
-__device__ __forceinline__ bool item_trace(const StepArgs& args, uint32_t i, const uint32_t*& tk) {
-  // read-only in this kernel and written by the previous one: the L1 path
-  // serves every CTA of an SM after the first (an L2 round trip each before)
-#if RKC_BCNT_STRIDE == 1
+// the step's per-bucket heavy counts (read-only in this kernel and written by
+// the previous one: the L1 path serves every CTA of an SM after the first)
+__device__ __forceinline__ void bucket_counts(const StepArgs& args, uint32_t (&cnt)[8]) {
   const uint4* cnt4 = reinterpret_cast<const uint4*>(args.p.bcnt + (args.step & 1u) * 8);
   const uint4 ca = __ldg(cnt4), cb = __ldg(cnt4 + 1);
-  const uint32_t cnt[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
-#else
-  const uint32_t* cp = args.p.bcnt + (args.step & 1u) * 8 * kBcntStride;
-  uint32_t cnt[8];
-#pragma unroll
-  for (uint32_t q = 0; q < 8; ++q) cnt[q] = __ldg(cp + q * kBcntStride);
-#endif
+  cnt[0] = ca.x; cnt[1] = ca.y; cnt[2] = ca.z; cnt[3] = ca.w;
+  cnt[4] = cb.x; cnt[5] = cb.y; cnt[6] = cb.z; cnt[7] = cb.w;
+}
+// bucketed item i of this step -> its ticket (false past the heavy count)
+__device__ __forceinline__ bool item_ticket(const StepArgs& args, const uint32_t (&cnt)[8], uint32_t i,
+                                            const uint32_t*& tk) {
   uint32_t acc = 0, bk = 8, off = 0;
 #pragma unroll
   for (uint32_t q = 0; q < 8; ++q) {
     const uint32_t c = cnt[q];
-    if (bk == 8 && i < acc + c) { bk = q; off = RKC_TICKET_REVERSE ? acc + c - 1 - i : i - acc; }
+    if (bk == 8 && i < acc + c) { bk = q; off = i - acc; }
     acc += c;
   }
   if (bk == 8) return false;
   tk = args.p.perm + ((size_t)bk * args.p.num_traces + off) * kTicketWords;
   return true;
 }
+__device__ __forceinline__ bool item_trace(const StepArgs& args, uint32_t i, const uint32_t*& tk) {
+  uint32_t cnt[8];
+  bucket_counts(args, cnt);
+  return item_ticket(args, cnt, i, tk);
+}
 
-// one heavy trace-step from its ticket word `tw` (lane l < 16 holds word l of
-// the ticket written by the light pass: the op in words 0..3, header words
-// 0..11 in 4..15, the trace id in place of (unused) header word 10): the
-// warp's whole op path
-__device__ RKC_RUN_ITEM_ATTR void run_item_body(const StepArgs& args, const uint4 opw, const uint32_t t,
+// one heavy trace-step from its ticket (written by the light pass: the op in
+// words 0..3, hot header words 0..11 in 4..15, the trace id in place of the
+// unused header word 10): op, trace id, header word `lane` (< 10) and the next
+// expiry step -- the warp's whole op path
+__device__ __forceinline__ void run_item_body(const StepArgs& args, const uint4 opw, const uint32_t t,
                                                 const uint32_t hw, const uint32_t next_exp) {
   const uint32_t lane = threadIdx.x & 31u;
   const PoolDev& p = args.p;
@@ -2628,13 +2257,10 @@ __device__ RKC_RUN_ITEM_ATTR void run_item_body(const StepArgs& args, const uint
   // hot header (lanes 0..15), the request record, the claim / object tables.
   const bool rq_op = (kind == OP_ADMIT || kind == OP_ADVANCE || kind == OP_COMPLETE ||
                       kind == OP_HIT_ADMIT) && a < p.Q;
-  // (big pools: an ADVANCE's allocation almost always evicts, and the
-  // eviction needs both tables: loaded here, off the crew's critical path)
-  const bool adv_tables = kBig && RKC_BIG_PRELOAD && kind == OP_ADVANCE;
   const bool want_cl = kind == OP_SUBMIT || kind == OP_DEMOTE || kind == OP_TOUCH ||
-                       kind == OP_COMPLETE || kind == OP_INSERT || kind == OP_HIT_ADMIT || adv_tables;
+                       kind == OP_COMPLETE || kind == OP_INSERT || kind == OP_HIT_ADMIT;
   const bool want_ob = kind == OP_SUBMIT || kind == OP_INSERT || kind == OP_COMPLETE ||
-                       kind == OP_TOUCH || kind == OP_HIT_ADMIT || adv_tables;
+                       kind == OP_TOUCH || kind == OP_HIT_ADMIT;
   uint32_t rqv = 0;
   if (rq_op && lane < 8) rqv = __ldcg(p.req + ((size_t)t * p.Q + a) * 8 + lane);
   uint4 c0 = make_uint4(0, 0, 0, 0), c1 = make_uint4(0, 0, 0, 0);
@@ -2664,11 +2290,7 @@ __device__ RKC_RUN_ITEM_ATTR void run_item_body(const StepArgs& args, const uint
     return;
   }
   if (lane < H_NWORDS) S.h[lane] = hw;
-#if RKC_TICKET_UNIFORM
   S.ctr[lane] = (lane == K_OPS && kind != OP_NOP) ? 1u : 0u;  // the op counts itself
-#else
-  S.ctr[lane] = 0;
-#endif
   if (lane < 4) { S.rc[lane] = 0; S.objdirty[lane] = 0; }
   if (lane < 8) S.rq[lane] = rqv;
   if (want_cl) {
@@ -2698,7 +2320,6 @@ __device__ RKC_RUN_ITEM_ATTR void run_item_body(const StepArgs& args, const uint
   __syncwarp();
   Op op{kind, a, (opw.x >> 16) & 0xFFu, opw.x >> 24, opw.y, opw.z, opw.w};
   if (args.step >= next_exp) expiry();
-  if (!RKC_TICKET_UNIFORM && kind != OP_NOP) ctr_add(K_OPS, 1);
   switch (kind) {
     case OP_NOP: break;
     case OP_SUBMIT: op_submit(op); break;
@@ -2716,16 +2337,6 @@ __device__ RKC_RUN_ITEM_ATTR void run_item_body(const StepArgs& args, const uint
   crew_exit();
 }
 
-// the ticket as one word per lane (lane l < 16 holds word l), spread by shuffles
-__device__ __forceinline__ void run_item_tw(const StepArgs& args, const uint32_t tw) {
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint4 opw = make_uint4(__shfl_sync(kFull, tw, 0), __shfl_sync(kFull, tw, 1),
-                               __shfl_sync(kFull, tw, 2), __shfl_sync(kFull, tw, 3));
-  const uint32_t t = __shfl_sync(kFull, tw, 14);
-  const uint32_t hsh = __shfl_sync(kFull, tw, (lane + 4) & 31u);
-  const uint32_t hw = lane < 10 ? hsh : 0u;  // hot header words 0..9 (10..15 unused)
-  run_item_body(args, opw, t, hw, __shfl_sync(kFull, hw, H_NEXT_EXPIRY));
-}
 __device__ __forceinline__ void run_item(const StepArgs& args, const uint32_t* tk) {
 #if RKC_BIG
   if (threadIdx.x >= 32) {  // crew helpers: block-pass slices until the leader is done
@@ -2734,7 +2345,6 @@ __device__ __forceinline__ void run_item(const StepArgs& args, const uint32_t* t
   }
 #endif
   const uint32_t lane = threadIdx.x & 31u;
-#if RKC_TICKET_UNIFORM
   // the op (words 0..3) and words 12..15 {next expiry, event count, trace, -}
   // as warp-uniform 16-B loads, header words 0..9 one per lane: independent
   // loads, no shuffles
@@ -2743,9 +2353,6 @@ __device__ __forceinline__ void run_item(const StepArgs& args, const uint32_t* t
   const uint4 tail = __ldg(tk4 + 3);
   const uint32_t hw = lane < 10 ? __ldg(tk + 4 + lane) : 0u;
   run_item_body(args, opw, tail.z, hw, tail.x);
-#else
-  run_item_tw(args, lane < kTicketWords ? __ldg(tk + lane) : 0u);
-#endif
 }
 
 // K1: warp w of CTA b -> the (b * kWarpsPerCta + w)-th trace of the op-kind
@@ -2765,27 +2372,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * kCrew * 32, kMinCtas)
 rkc_step_kernel(const __grid_constant__ StepArgs args) {
   pdl_wait();
   const uint32_t* tk;
-#if !RKC_BIG && RKC_ITEMS_PER_CTA == 2
-  // two consecutive items per one-warp CTA: the second ticket is loaded
-  // before the first item runs, so its latency hides behind the first item
-  const uint32_t i0 = blockIdx.x * 2;
-  if (!item_trace(args, i0, tk)) return;
-  const uint32_t* tk1;
-  const bool two = item_trace(args, i0 + 1, tk1);
-  const uint32_t lane = threadIdx.x & 31u;
-  uint32_t tw = lane < kTicketWords ? __ldg(tk + lane) : 0u;
-  const uint32_t tw1 = (two && lane < kTicketWords) ? __ldg(tk1 + lane) : 0u;
-#pragma unroll 1
-  for (uint32_t it = 0;; ++it) {
-    run_item_tw(args, tw);
-    if (it == 1 || !two) break;
-    __syncwarp();
-    tw = tw1;
-  }
-#else
   if (!item_trace(args, blockIdx.x * kWarpsPerCta + (kWarpsPerCta == 1 ? 0u : (threadIdx.x >> 5)), tk)) return;
   run_item(args, tk);
-#endif
 }
 
 #if !RKC_BIG
@@ -2839,7 +2427,7 @@ static cudaError_t launch_pdl(Kernel kernel, uint32_t grid, uint32_t block, cuda
 // host launcher: one launch = one lockstep step over all traces
 cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, cudaStream_t st) {
   StepArgs args{p, reinterpret_cast<const uint4*>(ops_step), step};
-  const uint32_t lct = (p.num_traces + kLightThreads * RKC_LIGHT_ILP - 1) / (kLightThreads * RKC_LIGHT_ILP);
+  const uint32_t lct = (p.num_traces + kLightThreads - 1) / kLightThreads;
 // one light thread per trace (round 2: the former cap of 16 CTAs per SM, i.e. 3.3 traces per
 // thread at c5, measured 1 % slower per lockstep step: profiles/r02/experiments.md)
 #ifndef RKC_LIGHT_MAX_CTAS
@@ -2852,7 +2440,7 @@ cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, c
     e = launch_pdl(rkc_step_kernel, (p.num_traces + kWarpsPerCta - 1) / kWarpsPerCta, kWarpsPerCta * kCrew * 32, st, args);
 #else
   if (e == cudaSuccess)
-    e = launch_pdl(rkc_step_kernel, (kMainItems(p.num_traces) + kWarpsPerCta * RKC_ITEMS_PER_CTA - 1) / (kWarpsPerCta * RKC_ITEMS_PER_CTA), kWarpsPerCta * 32, st, args);
+    e = launch_pdl(rkc_step_kernel, (kMainItems(p.num_traces) + kWarpsPerCta - 1) / kWarpsPerCta, kWarpsPerCta * 32, st, args);
   if (e == cudaSuccess) e = launch_pdl(rkc_step_overflow_kernel, kOverflowCtas(p.num_traces), 32, st, args);
 #endif
   return e;
