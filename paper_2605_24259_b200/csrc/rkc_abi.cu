@@ -6,6 +6,7 @@
 #include <nvtx3/nvToolsExt.h>
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -14,9 +15,19 @@
 #include "../../include/rkc.h"
 #include "rkc_internal.cuh"
 
+#ifndef RKC_GRID_PACING
+#define RKC_GRID_PACING 1   // round 2: c5 927 -> 902 us per lockstep step, c8 123 -> 114
+#endif
+#ifndef RKC_PACE_SHIFT
+#define RKC_PACE_SHIFT 5
+#endif
+#ifndef RKC_PACE_MAX
+#define RKC_PACE_MAX 0
+#endif
 namespace rkc {
 #define RKC_DECLARE_STEP(ns) \
-  namespace ns { cudaError_t launch_step(const PoolDev&, const void*, uint32_t, cudaStream_t); }
+  namespace ns { cudaError_t launch_step(const PoolDev&, const void*, uint32_t, cudaStream_t, uint32_t, \
+                                         unsigned long long*, uint32_t); }
 RKC_DECLARE_STEP(small_o64)
 RKC_DECLARE_STEP(small_o128)
 RKC_DECLARE_STEP(big_o64)
@@ -28,11 +39,15 @@ std::atomic<unsigned long long> g_launches{0};  // kernels this library launched
 // small pools), from the build of the pool's size class: <= 1024 blocks (keys
 // staged in shared memory) or more, and <= 64 object slots (32 resident CTAs
 // per SM) or up to 128
-static cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, cudaStream_t st) {
+static cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, cudaStream_t st,
+                               uint32_t main_items = 0, unsigned long long* host_heavy = nullptr,
+                               uint32_t tag_hi = 0) {
   g_launches += p.NS <= 1024 ? 3 : 2;
   if (p.NS <= 1024)
-    return p.O <= 64 ? small_o64::launch_step(p, ops_step, step, st) : small_o128::launch_step(p, ops_step, step, st);
-  return p.O <= 64 ? big_o64::launch_step(p, ops_step, step, st) : big_o128::launch_step(p, ops_step, step, st);
+    return p.O <= 64 ? small_o64::launch_step(p, ops_step, step, st, main_items, host_heavy, tag_hi)
+                     : small_o128::launch_step(p, ops_step, step, st, main_items, host_heavy, tag_hi);
+  return p.O <= 64 ? big_o64::launch_step(p, ops_step, step, st, main_items, host_heavy, tag_hi)
+                   : big_o128::launch_step(p, ops_step, step, st, main_items, host_heavy, tag_hi);
 }
 cudaError_t launch_conformance_array(const void* events, const uint32_t* offsets, uint32_t T,
                                      const uint8_t* final_states, uint32_t C, const uint8_t* lowering,
@@ -63,6 +78,13 @@ struct rkc_pool {
   cudaEvent_t ev_copied[2] = {nullptr, nullptr};
   cudaEvent_t ev_free[2] = {nullptr, nullptr};
   std::vector<void*> allocs;
+  // grid pacing (small pools): the step kernel publishes each step's heavy
+  // count into this mapped host ring; rkc_step_batch sizes the one-warp step
+  // grid of step s from the count of step s - kPaceLag (plus a margin)
+  // instead of launching 9/16 of the traces every step
+  unsigned long long* heavy_host = nullptr;  // [64] (step << 32) | count, mapped
+  unsigned long long* heavy_dev = nullptr;   // its device alias
+  uint32_t pace_epoch = 0;                   // rkc_step_batch calls (tags the ring entries)
   uint64_t step = 0;
   uint32_t stage_calls = 0;      // staging calls since the last step
   bool staged_any = false;
@@ -320,6 +342,9 @@ void free_all(rkc_pool* p) {
     if (p->ev_free[i]) cudaEventDestroy(p->ev_free[i]);
   }
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+  if (p->heavy_host) cudaFreeHost(p->heavy_host);
+  p->heavy_host = nullptr;
+  p->heavy_dev = nullptr;
 }
 
 // device staging for host outputs of rkc_telemetry_read: kept across calls
@@ -488,6 +513,18 @@ rkc_status rkc_pool_create(const rkc_pool_config* config, const rkc_trace_config
       free_all(p); delete p; return RKC_E_CUDA;
     }
   }
+  if (p->d.NS <= 1024) {  // grid pacing ring (small pools; absent: the fixed 9/16 grid)
+    if (cudaHostAlloc((void**)&p->heavy_host, 64 * sizeof(unsigned long long), cudaHostAllocMapped) ==
+            cudaSuccess &&
+        cudaHostGetDevicePointer((void**)&p->heavy_dev, p->heavy_host, 0) == cudaSuccess) {
+      for (int i = 0; i < 64; ++i) p->heavy_host[i] = ~0ull;
+    } else {
+      cudaGetLastError();
+      if (p->heavy_host) cudaFreeHost(p->heavy_host);
+      p->heavy_host = nullptr;
+      p->heavy_dev = nullptr;
+    }
+  }
   if ((s = run_init(p, 0)) != RKC_OK || cudaDeviceSynchronize() != cudaSuccess) {
     free_all(p); delete p; return s ? s : RKC_E_CUDA;
   }
@@ -541,6 +578,56 @@ rkc_status rkc_op_stage(rkc_pool* pool, const rkc_trace_op* ops, uint32_t n, int
   return stage_common(pool, stage_generic_kernel, ops, n, on_device, (cudaStream_t)stream, false);
 }
 
+// Grid pacing for small pools: the one-warp step grid of step s is sized from
+// the heavy count the step kernel of step s - kPaceLag published (mapped host
+// ring), plus a margin; items past it run on the overflow kernel, so a short
+// estimate costs time, never correctness.  The first kPaceLag steps of a batch,
+// or a ring that does not answer within a second, use the fixed default grid.
+namespace {
+constexpr uint32_t kPaceLag = 3;
+struct Pacer {
+  rkc_pool* pool;
+  uint64_t first;        // absolute step of the batch's first launch
+  bool on = false;
+  uint32_t last_h = 0;
+  uint32_t hist[4] = {0, 0, 0, 0};
+  uint32_t nh = 0;
+  uint32_t tag_hi;       // this batch's epoch << 16
+  Pacer(rkc_pool* p, uint64_t s0)
+      : pool(p), first(s0), on(p->heavy_host != nullptr && RKC_GRID_PACING),
+        tag_hi((++p->pace_epoch & 0xFFFFu) << 16) {}
+  // main_items for the launch of absolute step s (0: the default grid)
+  uint32_t main_items(uint64_t s) {
+    if (!on || s < first + kPaceLag) return 0;
+    const uint64_t src = s - kPaceLag;
+    volatile unsigned long long* slot = pool->heavy_host + (src & 63u);
+    const auto t0 = std::chrono::steady_clock::now();
+    unsigned long long v;
+    for (uint32_t spin = 0;; ++spin) {
+      v = *slot;
+      if ((v >> 32) == (tag_hi | (src & 0xFFFFu)) && v != ~0ull) break;
+      if ((spin & 1023u) == 1023u &&
+          std::chrono::steady_clock::now() - t0 > std::chrono::seconds(1)) {
+        on = false;  // no answer: the default grid for the rest of this batch
+        return 0;
+      }
+    }
+    const uint32_t h = (uint32_t)v, T = pool->d.num_traces;
+    // margin: 1/2^RKC_PACE_SHIFT of the traces plus twice the growth over the
+    // lag (pools fill); the base is the largest of the last few counts
+    const uint32_t grow = h > last_h ? (h - last_h) * 2 * kPaceLag : 0u;
+    last_h = h;
+    hist[nh++ & 3u] = h;
+    uint32_t hb = h;
+    if (RKC_PACE_MAX)
+      for (uint32_t i = 0; i < (nh < 4 ? nh : 4u); ++i) hb = hist[i] > hb ? hist[i] : hb;
+    const uint64_t m = (uint64_t)hb + (T >> RKC_PACE_SHIFT) + grow + 1024;
+    return (uint32_t)(m < T ? m : T);
+  }
+  unsigned long long* ring() const { return on ? pool->heavy_dev : nullptr; }
+};
+}  // namespace
+
 rkc_status rkc_step_batch(rkc_pool* pool, const rkc_op* ops, uint32_t num_steps, int on_device,
                           void* stream) {
   if (!pool) return RKC_E_INVAL;
@@ -561,9 +648,13 @@ rkc_status rkc_step_batch(rkc_pool* pool, const rkc_op* ops, uint32_t num_steps,
   }
   if (pool->staged_any) return RKC_E_STATE;  // staged ops pending: run them first
   if (num_steps == 0) return RKC_OK;
+  Pacer pace(pool, pool->step);
   if (on_device) {
-    for (uint32_t s = 0; s < num_steps; ++s)
-      CUDA_TRY(launch_step(pool->d, ops + (size_t)s * T, (uint32_t)(pool->step + s), st));
+    for (uint32_t s = 0; s < num_steps; ++s) {
+      const uint32_t mi = pace.main_items(pool->step + s);
+      CUDA_TRY(launch_step(pool->d, ops + (size_t)s * T, (uint32_t)(pool->step + s), st, mi, pace.ring(),
+                           pace.tag_hi));
+    }
     pool->step += num_steps;
     return RKC_OK;
   }
@@ -595,9 +686,11 @@ rkc_status rkc_step_batch(rkc_pool* pool, const rkc_op* ops, uint32_t num_steps,
                              cudaMemcpyHostToDevice, pool->copy_stream));
     CUDA_TRY(cudaEventRecord(pool->ev_copied[buf], pool->copy_stream));
     CUDA_TRY(cudaStreamWaitEvent(st, pool->ev_copied[buf], 0));
-    for (uint32_t s = 0; s < n; ++s)
+    for (uint32_t s = 0; s < n; ++s) {
+      const uint32_t mi = pace.main_items(pool->step + done + s);
       CUDA_TRY(launch_step(pool->d, pool->replay_buf[buf] + (size_t)s * T,
-                           (uint32_t)(pool->step + done + s), st));
+                           (uint32_t)(pool->step + done + s), st, mi, pace.ring(), pace.tag_hi));
+    }
     CUDA_TRY(cudaEventRecord(pool->ev_free[buf], st));
     done += n;
     buf ^= 1;

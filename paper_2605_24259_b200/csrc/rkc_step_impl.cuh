@@ -1087,6 +1087,12 @@ __device__ RKC_COUNT_ATTR uint32_t count_le(uint32_t T) {
 // 32 staged keys are <= T (bit 4j + e for block (j*32 + lane)*4 + e), so the
 // probe that hits the exact count hands the taken set to the apply step
 // without a second pass over the keys.
+#ifndef RKC_CTR_LANES
+#define RKC_CTR_LANES 0
+#endif
+#ifndef RKC_SPREAD_FILL
+#define RKC_SPREAD_FILL 0
+#endif
 #ifndef RKC_MASK_APPLY
 #define RKC_MASK_APPLY 1
 #endif
@@ -1468,11 +1474,22 @@ __device__ RKC_EVICT_ATTR void alloc_evict(uint32_t k, uint32_t owner, bool inse
   rel = __reduce_add_sync(kFull, rel);
   clm = __reduce_add_sync(kFull, clm);
   hset(H_FREE, 0);
+#if RKC_CTR_LANES
+  {  // the five counters of an evicting allocation, one lane per counter word
+    const uint32_t l = lane_id();
+    const uint32_t add = l == K_VICTIMS_ORDINARY ? ord : l == K_VICTIMS_AFTER_RELEASE ? rel :
+                         l == K_VICTIMS_CLAIMED ? clm : l == K_BLOCKS_ALLOCATED ? k :
+                         l == K_ALLOCATIONS ? 1u : 0u;
+    S.ctr[l] += add;
+    __syncwarp();
+  }
+#else
   ctr_add(K_VICTIMS_ORDINARY, ord);
   ctr_add(K_VICTIMS_AFTER_RELEASE, rel);
   ctr_add(K_VICTIMS_CLAIMED, clm);
   ctr_add(K_BLOCKS_ALLOCATED, k);
   ctr_add(K_ALLOCATIONS, 1);
+#endif
   if (ord + rel + clm > 0) {
     emit(EV_VICTIMS, owner, insert ? 1u : 0u, 0, ord, rel, clm, k);
     flag_set(F_POST);
@@ -2001,6 +2018,9 @@ struct StepArgs {
   PoolDev p;
   const uint4* ops;     // this step's row: [num_traces]
   uint32_t step;        // global step index of this launch
+  uint32_t main_items;  // small pools: items of the one-warp step grid (the rest: overflow kernel)
+  unsigned long long* host_heavy;  // mapped host ring [64]: (tag << 32) | heavy count, or null
+  uint32_t tag_hi;      // batch epoch << 16 (the low 16 bits of the tag: the step)
 };
 
 // op kind -> dispatch bucket: heavy block-scanning ops first, cheap ones last
@@ -2372,8 +2392,45 @@ __global__ void __launch_bounds__(kWarpsPerCta * kCrew * 32, kMinCtas)
 rkc_step_kernel(const __grid_constant__ StepArgs args) {
   pdl_wait();
   const uint32_t* tk;
+  if (args.host_heavy && blockIdx.x == 0 && threadIdx.x == 0) {
+    // this step's heavy count, published to the host (which sizes the step
+    // grid a few steps ahead from it: rkc_abi.cu grid pacing)
+    uint32_t cnt[8];
+    bucket_counts(args, cnt);
+    uint32_t H = 0;
+#pragma unroll
+    for (uint32_t q = 0; q < 8; ++q) H += cnt[q];
+    volatile unsigned long long* slot = args.host_heavy + (args.step & 63u);
+    *slot = ((unsigned long long)(args.tag_hi | (args.step & 0xFFFFu)) << 32) | H;
+    __threadfence_system();
+  }
+#if !RKC_BIG && RKC_SPREAD_FILL
+  // While pools fill, most of the grid finds no item (H heavy items, G CTAs):
+  // those empty CTAs would queue behind the last real one as a dispatch-bound
+  // tail.  When H < 3/4 G the items are spread evenly over the grid (CTA b
+  // takes item floor(b H / G) if it is the first CTA mapping to it), so the
+  // empty CTAs retire between the busy ones; items stay in bucket order.
+  // (Spreading at the steady state, H ~ G, measured 2.5 % slower.)
+  uint32_t cnt[8];
+  bucket_counts(args, cnt);
+  uint32_t H = 0;
+#pragma unroll
+  for (uint32_t q = 0; q < 8; ++q) H += cnt[q];
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  uint32_t i = b;
+  if ((uint64_t)H * 4 < (uint64_t)G * 3) {
+    const uint64_t x = (uint64_t)b * H;
+    i = (uint32_t)((double)x / (double)G);
+    while ((uint64_t)(i + 1) * G <= x) ++i;   // exact floor(b H / G)
+    while ((uint64_t)i * G > x) --i;
+    if (b > 0 && (uint64_t)(b - 1) * H >= (uint64_t)i * G) return;  // not the first CTA of item i
+  }
+  if (!item_ticket(args, cnt, i, tk)) return;
+  run_item(args, tk);
+#else
   if (!item_trace(args, blockIdx.x * kWarpsPerCta + (kWarpsPerCta == 1 ? 0u : (threadIdx.x >> 5)), tk)) return;
   run_item(args, tk);
+#endif
 }
 
 #if !RKC_BIG
@@ -2389,17 +2446,17 @@ __host__ __device__ constexpr uint32_t kMainItems(uint32_t T) {  // RKC_MAIN_SIX
 #ifndef RKC_OVF_MAX_CTAS
 #define RKC_OVF_MAX_CTAS (148u * 16u)
 #endif
-__host__ __device__ constexpr uint32_t kOverflowCtas(uint32_t T) {
+__host__ __device__ constexpr uint32_t kOverflowCtas(uint32_t T, uint32_t main) {
   // capped: every overflow CTA is dispatched every step even when no item
   // overflows (~0.5 ns each), and c5 would otherwise launch 27k of them
-  return (T - kMainItems(T)) / 16 > 592
-             ? ((T - kMainItems(T)) / 16 < (uint32_t)(RKC_OVF_MAX_CTAS) ? (T - kMainItems(T)) / 16
-                                                                        : (uint32_t)(RKC_OVF_MAX_CTAS))
+  return (T - main) / 16 > 592
+             ? ((T - main) / 16 < (uint32_t)(RKC_OVF_MAX_CTAS) ? (T - main) / 16
+                                                               : (uint32_t)(RKC_OVF_MAX_CTAS))
              : 592;
 }
 __global__ void __launch_bounds__(32) rkc_step_overflow_kernel(const __grid_constant__ StepArgs args) {
   pdl_wait();
-  for (uint32_t i = kMainItems(args.p.num_traces) + blockIdx.x;; i += gridDim.x) {
+  for (uint32_t i = args.main_items + blockIdx.x;; i += gridDim.x) {
     const uint32_t* tk;
     if (!item_trace(args, i, tk)) return;
     run_item(args, tk);
@@ -2425,8 +2482,17 @@ static cudaError_t launch_pdl(Kernel kernel, uint32_t grid, uint32_t block, cuda
 }
 
 // host launcher: one launch = one lockstep step over all traces
-cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, cudaStream_t st) {
-  StepArgs args{p, reinterpret_cast<const uint4*>(ops_step), step};
+// main_items: the one-warp step grid of a small pool (0: the default
+// kMainItems(T)); host_heavy: where the step kernel publishes the heavy count
+cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, cudaStream_t st,
+                        uint32_t main_items, unsigned long long* host_heavy, uint32_t tag_hi) {
+#if RKC_BIG
+  const uint32_t main = p.num_traces;
+#else
+  const uint32_t main = main_items ? (main_items < p.num_traces ? main_items : p.num_traces)
+                                   : kMainItems(p.num_traces);
+#endif
+  StepArgs args{p, reinterpret_cast<const uint4*>(ops_step), step, main, host_heavy, tag_hi};
   const uint32_t lct = (p.num_traces + kLightThreads - 1) / kLightThreads;
 // one light thread per trace (round 2: the former cap of 16 CTAs per SM, i.e. 3.3 traces per
 // thread at c5, measured 1 % slower per lockstep step: profiles/r02/experiments.md)
@@ -2440,8 +2506,8 @@ cudaError_t launch_step(const PoolDev& p, const void* ops_step, uint32_t step, c
     e = launch_pdl(rkc_step_kernel, (p.num_traces + kWarpsPerCta - 1) / kWarpsPerCta, kWarpsPerCta * kCrew * 32, st, args);
 #else
   if (e == cudaSuccess)
-    e = launch_pdl(rkc_step_kernel, (kMainItems(p.num_traces) + kWarpsPerCta - 1) / kWarpsPerCta, kWarpsPerCta * 32, st, args);
-  if (e == cudaSuccess) e = launch_pdl(rkc_step_overflow_kernel, kOverflowCtas(p.num_traces), 32, st, args);
+    e = launch_pdl(rkc_step_kernel, (main + kWarpsPerCta - 1) / kWarpsPerCta, kWarpsPerCta * 32, st, args);
+  if (e == cudaSuccess) e = launch_pdl(rkc_step_overflow_kernel, kOverflowCtas(p.num_traces, main), 32, st, args);
 #endif
   return e;
 }
