@@ -61,6 +61,9 @@ constexpr int kCrewUnroll = RKC_CREW_UNROLL;  // block vectors in flight per lan
 #endif
 constexpr uint32_t kObjMax = RKC_OMAX;
 
+#ifndef RKC_LIGHT_THREAD_TAKE
+#define RKC_LIGHT_THREAD_TAKE 0
+#endif
 #ifndef RKC_LIGHT_RANKED
 #define RKC_LIGHT_RANKED 1   // free-only takes: one rank per lane instead of a bit loop per word
 #endif
@@ -2141,6 +2144,38 @@ __global__ void __launch_bounds__(kLightThreads, RKC_LIGHT_MIN_CTAS) rkc_light_k
         }
       }
     }
+#if RKC_LIGHT_THREAD_TAKE
+    // free-only allocations, one thread per trace: the `need` lowest-id free
+    // blocks (bitmap words four at a time, lowest first), positions live.. in
+    // block-id order (G24).  While pools fill the free blocks are a run at the
+    // end of the pool, so a take usually reads one or two 16-B groups; the
+    // threads of a warp run their traces side by side instead of in turn.
+    if (fa) {
+      uint32_t* fb = p.fbm + (size_t)t * (p.NS / 32);
+      uint32_t* key = p.key + (size_t)t * p.NS;
+      uint32_t* meta = p.meta + (size_t)t * p.NS;
+      uint32_t got = 0;
+      for (uint32_t g = 0; g < p.NS / 128 && got < fa_need; ++g) {
+        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(fb) + g);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t word = el(v, e);
+          if (word == 0 || got >= fa_need) continue;
+          const uint32_t c = __popc(word);
+          const uint32_t take = min(c, fa_need - got);
+          uint32_t tw = take == c ? word : word & ((1u << nth_set_bit(word, take + 1)) - 1u);
+          const uint32_t wi = g * 4 + e;
+          fb[wi] = word & ~tw;
+          for (; tw; tw &= tw - 1) {
+            const uint32_t b = wi * 32 + __ffs(tw) - 1;
+            meta[b] = meta_make(kResActive, fa_owner, fa_live + got++);
+            key[b] = kKeyActive;
+          }
+        }
+      }
+    }
+    if (false)
+#endif
     // free-only allocations, one trace at a time across the warp (lane = free
     // bitmap word): the `need` lowest-id free blocks, positions live.. in
     // block-id order (G24)
