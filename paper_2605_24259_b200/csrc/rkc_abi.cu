@@ -21,6 +21,12 @@
 #ifndef RKC_PACE_SHIFT
 #define RKC_PACE_SHIFT 6   // margin 1/64 of the traces (1/32: +0.4 %, 1/16: +2.2 % on c5)
 #endif
+#ifndef RKC_PACE_LAG
+#define RKC_PACE_LAG 3   // steps between a published heavy count and the grid it sizes
+#endif
+#ifndef RKC_PACE_FLOOR
+#define RKC_PACE_FLOOR 1024   // constant part of the margin (items)
+#endif
 #ifndef RKC_PACE_MAX
 #define RKC_PACE_MAX 0
 #endif
@@ -589,7 +595,7 @@ rkc_status rkc_op_stage(rkc_pool* pool, const rkc_trace_op* ops, uint32_t n, int
 // estimate costs time, never correctness.  The first kPaceLag steps of a batch,
 // or a ring that does not answer within a second, use the fixed default grid.
 namespace {
-constexpr uint32_t kPaceLag = 3;
+constexpr uint32_t kPaceLag = RKC_PACE_LAG;
 struct Pacer {
   rkc_pool* pool;
   uint64_t first;        // absolute step of the batch's first launch
@@ -626,7 +632,7 @@ struct Pacer {
     uint32_t hb = h;
     if (RKC_PACE_MAX)
       for (uint32_t i = 0; i < (nh < 4 ? nh : 4u); ++i) hb = hist[i] > hb ? hist[i] : hb;
-    const uint64_t m = (uint64_t)hb + (T >> RKC_PACE_SHIFT) + grow + 1024;
+    const uint64_t m = (uint64_t)hb + (T >> RKC_PACE_SHIFT) + grow + RKC_PACE_FLOOR;
     return (uint32_t)(m < T ? m : T);
   }
   unsigned long long* ring() const { return on ? pool->heavy_dev : nullptr; }

@@ -1,0 +1,15 @@
+#!/bin/bash
+# Session-3 A/B #16: rank-parallel block selection instead of a shared-memory list in the mask apply.
+OUT=gpurun_out; mkdir -p $OUT
+: > $OUT/ab_s3p.txt
+RKC_LIB=exp_libs/s1_ranksel.so timeout 1200 python -m pytest tests -m gpu -x -q > $OUT/par_s1.log 2>&1; echo "rc=$?" >> $OUT/par_s1.log
+for round in 1 2; do
+  for lib in q3_pace64 s1_ranksel; do
+    RKC_LIB=exp_libs/$lib.so timeout 600 python tools/step_timing.py --traces 1000000 --reps 3 --tag c5_$lib >> $OUT/ab_s3p.txt 2>&1
+    for c in 3 6 8; do
+      RKC_LIB=exp_libs/$lib.so timeout 300 python tools/step_timing.py --config $c --tag c${c}_$lib >> $OUT/ab_s3p.txt 2>&1
+    done
+  done
+done
+tail -3 $OUT/par_s1.log
+cat $OUT/ab_s3p.txt
