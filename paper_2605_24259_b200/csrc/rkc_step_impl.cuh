@@ -61,9 +61,6 @@ constexpr int kCrewUnroll = RKC_CREW_UNROLL;  // block vectors in flight per lan
 #endif
 constexpr uint32_t kObjMax = RKC_OMAX;
 
-#ifndef RKC_STATS_MAX
-#define RKC_STATS_MAX 0   // big pools: the stats pass also finds the largest class-1 key (density-based first probe)
-#endif
 #ifndef RKC_LIGHT_RANKED
 #define RKC_LIGHT_RANKED 1   // free-only takes: one rank per lane instead of a bit loop per word
 #endif
@@ -424,7 +421,7 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
   uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
   switch (kind) {
     case JOB_STATS: {  // class-1 count, smallest non-free key - 2^30 (see alloc_evict)
-      uint32_t md = kFull, mx = 0;
+      uint32_t md = kFull;
 #pragma unroll(kCrewUnroll)
       for (uint32_t j = j0; j < j1; ++j) {
         crew_pf(key4, j, j1);
@@ -434,12 +431,10 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
           const uint32_t d = el(v, e) - kC1;
           r0 += d < kC1 ? 1u : 0u;
           md = min(md, d);
-          if (RKC_STATS_MAX) mx = max(mx, d < kC1 ? d : 0u);  // largest class-1 key - 2^30
         }
       }
       r0 = __reduce_add_sync(kFull, r0);
       r1 = __reduce_min_sync(kFull, md);
-      if (RKC_STATS_MAX) r2 = __reduce_max_sync(kFull, mx);
       break;
     }
     case JOB_COUNT: {  // #{key <= T}
@@ -1222,7 +1217,7 @@ __device__ RKC_EVICT_ATTR void alloc_evict(uint32_t k, uint32_t owner, bool inse
   // #{d < 2^30} the class-1 count (the class-2 minimum is needed only when
   // class 1 cannot cover the shortfall: a second pass then)
   constexpr uint32_t kC1 = 1u << kClassShift;
-  uint32_t c1 = 0, md = kFull, c1max = 0;
+  uint32_t c1 = 0, md = kFull;
   auto stat = [&](const uint4& v) {
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -1252,12 +1247,6 @@ __device__ RKC_EVICT_ATTR void alloc_evict(uint32_t k, uint32_t owner, bool inse
     crew_run(JOB_STATS);
     c1 = lane_id() == 0 ? crew_sum(0) : 0u;  // summed over the warp below
     md = crew_min(1);
-    if (RKC_STATS_MAX) {
-      uint32_t m = 0;
-#pragma unroll
-      for (uint32_t w = 0; w < kCrew; ++w) m = max(m, S.red[w][2]);
-      c1max = m;
-    }
 #else
     for (uint32_t j = 0; j < nv; ++j) stat(__ldcg(key4 + j * 32 + lane));
 #endif
@@ -1314,15 +1303,6 @@ __device__ RKC_EVICT_ATTR void alloc_evict(uint32_t k, uint32_t owner, bool inse
         d = max(d, 2 * (uint64_t)last_d);
         last_d = (uint32_t)min(d, (uint64_t)0xFFFFFFFFu);
         m = (uint32_t)min((uint64_t)lo + d, (uint64_t)top);
-      } else if (!staged && RKC_STATS_MAX && it == 0 && top == (2u << kClassShift) - 1 &&
-                 c1 > 0) {
-        // big pools, class 1: the first probe from the class-1 key density
-        // (count over [min, max]), 1/8 beyond it so it usually brackets
-        const float span = (float)(c1max - (lo0 + 1 - kC1)) + 1.0f;
-        const float df = fminf((float)(k - clo) * span * 1.125f / (float)c1, 4.0e9f);
-        const uint64_t d = (uint64_t)__float2uint_rz(df) + 1;
-        m = (uint32_t)min((uint64_t)lo + d, (uint64_t)top);
-        last_d = (uint32_t)min(d, (uint64_t)0xFFFFFFFFu);
       } else {
         const uint64_t d = (uint64_t)(k - clo) * mult;
         m = (uint32_t)min((uint64_t)lo + d, (uint64_t)top);

@@ -19,7 +19,7 @@ for c in c5 c3 c4 c6 c8; do
   timeout 1500 python bench.py --config $c > $OUT/bench_$c.json 2> $OUT/bench_$c.err; echo "rc=$?" >> $OUT/bench_$c.err
 done
 timeout 600 python bench.py --impl reference > $OUT/bench_reference.json 2> $OUT/bench_reference.err; echo "rc=$?" >> $OUT/bench_reference.err
-timeout 600 python bench.py --gpus 2 --steps 3 --warmup 3 > $OUT/bench_n2.json 2> $OUT/bench_n2.err; echo "rc=$?" >> $OUT/bench_n2.err
+for r in 1 2; do timeout 600 python bench.py --gpus 2 --steps 3 --warmup 3 > $OUT/bench_n2_$r.json 2> $OUT/bench_n2_$r.err; echo "rc=$?" >> $OUT/bench_n2_$r.err; done
 timeout 600 python tools/step_timing.py --traces 1000000 --reps 1 --per-step --tag c5_perstep > $OUT/perstep.txt 2>&1
 timeout 600 python tools/step_timing.py --traces 1000000 --reps 1 --nop --per-step --tag c5_nop >> $OUT/perstep.txt 2>&1
 timeout 2400 python tests/run_parity_1m.py --single-pool --chunk 50000 > $OUT/parity_1m_single_pool.log 2>&1; echo "rc=$?" >> $OUT/parity_1m_single_pool.log
