@@ -660,6 +660,13 @@ rkc_status rkc_step_batch(rkc_pool* pool, const rkc_op* ops, uint32_t num_steps,
   if (pool->staged_any) return RKC_E_STATE;  // staged ops pending: run them first
   if (num_steps == 0) return RKC_OK;
   Pacer pace(pool, pool->step);
+  {  // a stream under graph capture runs nothing until the graph launches: no counts to wait for
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      pace.on = false;
+    }
+  }
   if (on_device) {
     for (uint32_t s = 0; s < num_steps; ++s) {
       const uint32_t mi = pace.main_items(pool->step + s);
@@ -683,19 +690,32 @@ rkc_status rkc_step_batch(rkc_pool* pool, const rkc_op* ops, uint32_t num_steps,
   const size_t chunk = pool->replay_steps;
   CUDA_TRY(cudaEventRecord(pool->ev_free[0], st));
   CUDA_TRY(cudaEventRecord(pool->ev_free[1], st));
-  uint32_t done = 0;
-  int buf = 0;
   // chunk sizes ramp up (2, 8, 32, ... steps) so the first steps wait for a
-  // small copy only; each later copy overlaps the previous chunk's steps
+  // small copy only; the copy of chunk n + 1 is enqueued before the steps of
+  // chunk n are (the grid pacing below blocks the host while it launches
+  // them), so every copy overlaps the previous chunk's steps
   size_t ramp = 2;
-  while (done < num_steps) {
+  auto next_len = [&](uint32_t from) -> uint32_t {
     const size_t lim = ramp < chunk ? ramp : chunk;
     if (ramp < chunk) ramp *= 4;  // (capped: no overflow over many chunks)
-    const uint32_t n = (uint32_t)((num_steps - done) < lim ? (num_steps - done) : lim);
-    CUDA_TRY(cudaStreamWaitEvent(pool->copy_stream, pool->ev_free[buf], 0));
-    CUDA_TRY(cudaMemcpyAsync(pool->replay_buf[buf], ops + (size_t)done * T, (size_t)n * T * 16,
-                             cudaMemcpyHostToDevice, pool->copy_stream));
-    CUDA_TRY(cudaEventRecord(pool->ev_copied[buf], pool->copy_stream));
+    return (uint32_t)((num_steps - from) < lim ? (num_steps - from) : lim);
+  };
+  auto enqueue_copy = [&](uint32_t from, uint32_t n, int b) -> cudaError_t {
+    cudaError_t e = cudaStreamWaitEvent(pool->copy_stream, pool->ev_free[b], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(pool->replay_buf[b], ops + (size_t)from * T, (size_t)n * T * 16,
+                          cudaMemcpyHostToDevice, pool->copy_stream);
+    if (e == cudaSuccess) e = cudaEventRecord(pool->ev_copied[b], pool->copy_stream);
+    return e;
+  };
+  uint32_t done = 0;
+  int buf = 0;
+  uint32_t n = next_len(0);
+  CUDA_TRY(enqueue_copy(0, n, 0));
+  while (done < num_steps) {
+    const uint32_t nxt_from = done + n;
+    const uint32_t nxt = nxt_from < num_steps ? next_len(nxt_from) : 0u;
+    if (nxt) CUDA_TRY(enqueue_copy(nxt_from, nxt, buf ^ 1));
     CUDA_TRY(cudaStreamWaitEvent(st, pool->ev_copied[buf], 0));
     for (uint32_t s = 0; s < n; ++s) {
       const uint32_t mi = pace.main_items(pool->step + done + s);
@@ -704,6 +724,7 @@ rkc_status rkc_step_batch(rkc_pool* pool, const rkc_op* ops, uint32_t num_steps,
     }
     CUDA_TRY(cudaEventRecord(pool->ev_free[buf], st));
     done += n;
+    n = nxt;
     buf ^= 1;
   }
   pool->step += num_steps;

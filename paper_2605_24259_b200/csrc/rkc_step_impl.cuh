@@ -61,6 +61,9 @@ constexpr int kCrewUnroll = RKC_CREW_UNROLL;  // block vectors in flight per lan
 #endif
 constexpr uint32_t kObjMax = RKC_OMAX;
 
+#ifndef RKC_LIGHT_FA_FAST
+#define RKC_LIGHT_FA_FAST 0
+#endif
 #ifndef RKC_LIGHT_RANKED
 #define RKC_LIGHT_RANKED 1   // free-only takes: one rank per lane instead of a bit loop per word
 #endif
@@ -2166,6 +2169,23 @@ __global__ void __launch_bounds__(kLightThreads, RKC_LIGHT_MIN_CTAS) rkc_light_k
       const uint32_t live = __shfl_sync(kFull, fa_live, src), owner = __shfl_sync(kFull, fa_owner, src);
       uint32_t* fbm = p.fbm + (size_t)tt * (p.NS / 32);
       const uint32_t word = words[q];
+#if RKC_LIGHT_FA_FAST
+      {  // the lowest non-empty bitmap word holds all `need` blocks (pools filling: the free
+         // blocks are a run at the end of the pool): no scan, no search
+        const uint32_t fl = __ffs(__ballot_sync(kFull, word != 0)) - 1;
+        const uint32_t wf = __shfl_sync(kFull, word, fl & 31u);
+        const uint32_t cf = __popc(wf);
+        if (cf >= need) {
+          if (lane == fl) fbm[lane] = need == cf ? 0u : wf & ~((1u << nth_set_bit(wf, need + 1)) - 1u);
+          if (lane < need) {
+            const uint32_t b = fl * 32 + nth_set_bit(wf, lane + 1);
+            p.meta[(size_t)tt * p.NS + b] = meta_make(kResActive, owner, live + lane);
+            p.key[(size_t)tt * p.NS + b] = kKeyActive;
+          }
+          continue;
+        }
+      }
+#endif
       const uint32_t c = __popc(word);
       const uint32_t incl = warp_incl_scan(c, lane);
       const uint32_t before = incl - c;
