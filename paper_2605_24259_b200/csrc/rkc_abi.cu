@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -20,6 +21,9 @@
 #endif
 #ifndef RKC_PACE_SHIFT
 #define RKC_PACE_SHIFT 6   // margin 1/64 of the traces (1/32: +0.4 %, 1/16: +2.2 % on c5)
+#endif
+#ifndef RKC_PACE_HOST_OPS
+#define RKC_PACE_HOST_OPS 1   // pace the grid in the host-op-stream replay too
 #endif
 #ifndef RKC_PACE_LAG
 #define RKC_PACE_LAG 3   // steps between a published heavy count and the grid it sizes
@@ -617,8 +621,10 @@ struct Pacer {
     for (uint32_t spin = 0;; ++spin) {
       v = *slot;
       if ((v >> 32) == (tag_hi | (src & 0xFFFFu)) && v != ~0ull) break;
-      if ((spin & 1023u) == 1023u &&
-          std::chrono::steady_clock::now() - t0 > std::chrono::seconds(1)) {
+      // the host trails the GPU by kPaceLag steps (milliseconds): after a short
+      // spin, poll every 20 us instead of holding a core
+      if (spin >= 256) std::this_thread::sleep_for(std::chrono::microseconds(20));
+      if ((spin & 63u) == 63u && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(1)) {
         on = false;  // no answer: the default grid for the rest of this batch
         return 0;
       }
@@ -677,6 +683,7 @@ rkc_status rkc_step_batch(rkc_pool* pool, const rkc_op* ops, uint32_t num_steps,
     return RKC_OK;
   }
   // host op stream: double-buffered copies on the copy stream overlap the steps
+  if (!RKC_PACE_HOST_OPS) pace.on = false;
   if (!pool->replay_buf[0]) {
     size_t per_step = (size_t)T * 16;
     size_t steps = (256ull << 20) / per_step;  // 2 x 256 MB staging buffers
