@@ -31,9 +31,6 @@
 #ifndef RKC_PACE_FLOOR
 #define RKC_PACE_FLOOR 1024   // constant part of the margin (items)
 #endif
-#ifndef RKC_PACE_MAX
-#define RKC_PACE_MAX 0
-#endif
 namespace rkc {
 #define RKC_DECLARE_STEP(ns) \
   namespace ns { cudaError_t launch_step(const PoolDev&, const void*, uint32_t, cudaStream_t, uint32_t, \
@@ -605,8 +602,6 @@ struct Pacer {
   uint64_t first;        // absolute step of the batch's first launch
   bool on = false;
   uint32_t last_h = 0;
-  uint32_t hist[4] = {0, 0, 0, 0};
-  uint32_t nh = 0;
   uint32_t tag_hi;       // this batch's epoch << 16
   Pacer(rkc_pool* p, uint64_t s0)
       : pool(p), first(s0), on(p->heavy_host != nullptr && RKC_GRID_PACING),
@@ -631,14 +626,11 @@ struct Pacer {
     }
     const uint32_t h = (uint32_t)v, T = pool->d.num_traces;
     // margin: 1/2^RKC_PACE_SHIFT of the traces plus twice the growth over the
-    // lag (pools fill); the base is the largest of the last few counts
+    // lag (pools fill; the first estimate of a batch has no growth to go on and
+    // comes out generous)
     const uint32_t grow = h > last_h ? (h - last_h) * 2 * kPaceLag : 0u;
     last_h = h;
-    hist[nh++ & 3u] = h;
-    uint32_t hb = h;
-    if (RKC_PACE_MAX)
-      for (uint32_t i = 0; i < (nh < 4 ? nh : 4u); ++i) hb = hist[i] > hb ? hist[i] : hb;
-    const uint64_t m = (uint64_t)hb + (T >> RKC_PACE_SHIFT) + grow + RKC_PACE_FLOOR;
+    const uint64_t m = (uint64_t)h + (T >> RKC_PACE_SHIFT) + grow + RKC_PACE_FLOOR;
     return (uint32_t)(m < T ? m : T);
   }
   unsigned long long* ring() const { return on ? pool->heavy_dev : nullptr; }

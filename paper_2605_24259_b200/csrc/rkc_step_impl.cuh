@@ -1369,6 +1369,12 @@ __device__ RKC_EVICT_ATTR void alloc_evict(uint32_t k, uint32_t owner, bool inse
     }
     const uint32_t At = __shfl_sync(kFull, Ai, 31), Bt = __shfl_sync(kFull, Bi, 31);
     const uint32_t Ae = Ai - A, Be = Bi - B;
+    // the taken blocks' meta lines, pulled into L2 now: the list build below
+    // covers the HBM part of the victims' meta gather latency
+#pragma unroll 1
+    for (uint32_t j = 0; j < nv; ++j)
+      if ((M >> (4 * j)) & 15u)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint4*>(meta) + j * 32 + lane));
     __syncwarp();  // every lane's last probe has read the staged keys the list overwrites
     uint32_t vb = 0;
 #pragma unroll 1
