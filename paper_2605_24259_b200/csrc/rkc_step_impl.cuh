@@ -61,6 +61,12 @@ constexpr int kCrewUnroll = RKC_CREW_UNROLL;  // block vectors in flight per lan
 #endif
 constexpr uint32_t kObjMax = RKC_OMAX;
 
+#ifndef RKC_RC_REGS
+#define RKC_RC_REGS 0
+#endif
+#ifndef RKC_LIST_BITS
+#define RKC_LIST_BITS 1   // round 2: c5 -0.8 %
+#endif
 #ifndef RKC_LIGHT_FA_FAST
 #define RKC_LIGHT_FA_FAST 1   // round 2: c3 -0.7 %, c5 -0.3 %
 #endif
@@ -750,13 +756,24 @@ __device__ RKC_RECLASS_ATTR void flush_reclass_pass() {
   // one vector of block words per lane-step: rolled for staged-size pools
   // (instruction cache), unrolled for big ones (loads in flight); each
   // variant is its own function so the small-pool path stays compact
+#if RKC_RC_REGS
+  // the marked-object bitmap in registers (was one shared-memory load per element)
+  const uint32_t rcw0 = S.rc[0], rcw1 = S.rc[1], rcw2 = S.rc[2], rcw3 = S.rc[3];
+  auto in_rc = [&](uint32_t o) -> bool {
+    const uint32_t w = kObjMax <= 64 ? (o < 32 ? rcw0 : rcw1)
+                                     : (o < 64 ? (o < 32 ? rcw0 : rcw1) : (o < 96 ? rcw2 : rcw3));
+    return (w >> (o & 31u)) & 1u;
+  };
+#else
+  auto in_rc = [&](uint32_t o) -> bool { return in_reclass(o); };
+#endif
   auto vec_pass = [&](uint32_t j) {
     const uint4 mv = __ldcg(meta4 + j * 32 + lane_id());
     bool any = false;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const uint32_t m = el(mv, e);
-      any |= meta_res(m) == kResCached && in_reclass(meta_owner(m));
+      any |= meta_res(m) == kResCached && in_rc(meta_owner(m));
     }
     if (!any) return;
     const uint4 kv = __ldcg(key4 + j * 32 + lane_id());
@@ -765,7 +782,7 @@ __device__ RKC_RECLASS_ATTR void flush_reclass_pass() {
       const uint32_t m = el(mv, e);
       if (meta_res(m) != kResCached) continue;
       const uint32_t o = meta_owner(m);
-      if (!in_reclass(o)) continue;
+      if (!in_rc(o)) continue;
       const uint32_t pos = meta_pos(m);
       const bool pin = meta_pinned(m);  // shared by a running hit: class 3, not protected (G29)
       const uint32_t cls = (pin || pos < S.lim3[o]) ? 3u : (pos < S.lim2[o] ? 2u : 1u);
@@ -1376,6 +1393,21 @@ __device__ RKC_EVICT_ATTR void alloc_evict(uint32_t k, uint32_t owner, bool inse
       if ((M >> (4 * j)) & 15u)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint4*>(meta) + j * 32 + lane));
     __syncwarp();  // every lane's last probe has read the staged keys the list overwrites
+#if RKC_LIST_BITS
+    // one iteration per taken key of this lane (not per vector): the rank
+    // base of vector j is the byte sum of the totals of vectors < j (dp4a)
+#pragma unroll 1
+    for (uint32_t mm = M; mm; mm &= mm - 1) {
+      const uint32_t bit = __ffs(mm) - 1, j = bit >> 2, e = bit & 3u;
+      const uint32_t na = (j + 1) >> 1, nb = j >> 1;  // even / odd vectors below j
+      const uint32_t ma = na >= 4 ? 0xFFFFFFFFu : (1u << (8 * na)) - 1u;
+      const uint32_t mb = nb >= 4 ? 0xFFFFFFFFu : (1u << (8 * nb)) - 1u;
+      const uint32_t vbj = (uint32_t)__dp4a(At & ma, 0x01010101u, 0u) + (uint32_t)__dp4a(Bt & mb, 0x01010101u, 0u);
+      const uint32_t ex = (((j & 1u) ? Be : Ae) >> (8 * (j >> 1))) & 0xFFu;
+      const uint32_t within = __popc((M >> (4 * j)) & ((1u << e) - 1u));
+      list[vbj + ex + within] = block_of(j, e);
+    }
+#else
     uint32_t vb = 0;
 #pragma unroll 1
     for (uint32_t j = 0; j < nv; ++j) {
@@ -1388,6 +1420,7 @@ __device__ RKC_EVICT_ATTR void alloc_evict(uint32_t k, uint32_t owner, bool inse
       }
       vb += (((j & 1u) ? Bt : At) >> sh) & 0xFFu;
     }
+#endif
     __syncwarp();
     // one taken block per lane: FREE ones (meta residency FREE) are just
     // taken; cached ones are victims, attributed by their object's claim
