@@ -61,8 +61,11 @@ constexpr int kCrewUnroll = RKC_CREW_UNROLL;  // block vectors in flight per lan
 #endif
 constexpr uint32_t kObjMax = RKC_OMAX;
 
+#ifndef RKC_FINISH_VEC
+#define RKC_FINISH_VEC 0
+#endif
 #ifndef RKC_RC_REGS
-#define RKC_RC_REGS 0
+#define RKC_RC_REGS 1   // round 2: c5 -1.0 %, c3 -1.6 %
 #endif
 #ifndef RKC_LIST_BITS
 #define RKC_LIST_BITS 1   // round 2: c5 -0.8 %
@@ -96,7 +99,7 @@ struct alignas(16) Warp {      // the warp's shared memory (one warp per CTA)
   uint32_t t, step, nv, NS, C, Q, O, EPT;
   uint32_t h[H_NWORDS];        // hot header
   uint32_t rq[8];              // the request record of the current op
-  uint32_t nev, flags, cdirty, pad0;
+  alignas(16) uint32_t nev, flags, cdirty, pad0;  // one 16-B load in finish()
   uint32_t rc[4];              // objects whose blocks need reclassing
   uint32_t objdirty[4];
   uint32_t ctr[32];            // counter deltas of this step
@@ -603,6 +606,16 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
       break;
     }
     case JOB_RECLASS: {  // class bits of the marked objects' cached blocks (S.lim3 / S.lim2 / S.cnt3)
+#if RKC_RC_REGS
+      const uint32_t rcw0 = S.rc[0], rcw1 = S.rc[1], rcw2 = S.rc[2], rcw3 = S.rc[3];
+      auto in_rc = [&](uint32_t o) -> bool {
+        const uint32_t w = kObjMax <= 64 ? (o < 32 ? rcw0 : rcw1)
+                                         : (o < 64 ? (o < 32 ? rcw0 : rcw1) : (o < 96 ? rcw2 : rcw3));
+        return (w >> (o & 31u)) & 1u;
+      };
+#else
+      auto in_rc = [&](uint32_t o) -> bool { return in_reclass(o); };
+#endif
 #pragma unroll(kCrewUnroll)
       for (uint32_t j = j0; j < j1; ++j) {
         crew_pf(meta4, j, j1);
@@ -611,7 +624,7 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const uint32_t m = el(mv, e);
-          any |= meta_res(m) == kResCached && in_reclass(meta_owner(m));
+          any |= meta_res(m) == kResCached && in_rc(meta_owner(m));
         }
         if (!any) continue;
         const uint4 kv = __ldcg(key4 + j * 32 + lane);
@@ -620,7 +633,7 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
           const uint32_t m = el(mv, e);
           if (meta_res(m) != kResCached) continue;
           const uint32_t o = meta_owner(m);
-          if (!in_reclass(o)) continue;
+          if (!in_rc(o)) continue;
           const uint32_t pos = meta_pos(m);
           const bool pin = meta_pinned(m);  // shared by a running hit: class 3, not protected (G29)
           const uint32_t cls = (pin || pos < S.lim3[o]) ? 3u : (pos < S.lim2[o] ? 2u : 1u);
@@ -2023,6 +2036,46 @@ __device__ __noinline__ void finish() {
     post_op();
     flush_reclass();
   }
+#if RKC_FINISH_VEC
+  // the bookkeeping words in two 16-B loads ({nev, flags, cdirty}, objdirty[4]):
+  // one round trip instead of one per test below
+  __syncwarp();
+  const uint4 nf = *reinterpret_cast<const uint4*>(&S.nev);
+  const uint4 od = *reinterpret_cast<const uint4*>(S.objdirty);
+  bool hdr = (nf.y & F_HDR) != 0;
+  if (nf.y & F_CLAIMS_CHANGED) {
+    const uint32_t* r = S.cl[lane_id()];
+    const uint32_t ne = (lane_id() < S.C && live_state(r[0] & 0xFFu) && r[CF_D] > 0)
+                            ? (uint32_t)min((uint64_t)r[CF_DEC] + r[CF_D], (uint64_t)0xFFFFFFFFu)
+                            : 0xFFFFFFFFu;
+    const uint32_t m = __reduce_min_sync(kFull, ne);
+    if (lane_id() == 0) S.h[H_NEXT_EXPIRY] = m;
+    hdr = true;
+  }
+  if ((nf.z >> lane_id()) & 1u) {
+    uint4* cp = reinterpret_cast<uint4*>(S.clm + lane_id() * 8);
+    cp[0] = reinterpret_cast<const uint4*>(S.cl[lane_id()])[0];
+    cp[1] = reinterpret_cast<const uint4*>(S.cl[lane_id()])[1];
+  }
+  if (od.x | od.y | od.z | od.w) {
+    uint2* dst = S.obj;
+    const uint32_t O = S.O;
+#pragma unroll
+    for (uint32_t q = 0; q < kObjMax / 32; ++q) {
+      const uint32_t o = q * 32 + lane_id();
+      const uint32_t w = q == 0 ? od.x : q == 1 ? od.y : q == 2 ? od.z : od.w;
+      if (o < O && ((w >> lane_id()) & 1u)) dst[o] = make_uint2(S.obj0[o], S.lead[o]);
+    }
+  }
+  if (nf.x) {
+    if (lane_id() == 0) S.h[H_EVCOUNT] += nf.x;
+    hdr = true;
+  }
+  __syncwarp();
+  if (hdr && lane_id() < H_HOT) S.hdrp[lane_id()] = S.h[lane_id()];
+  const uint32_t d = S.ctr[lane_id()];
+  if (d) atomicAdd(S.ctrp + lane_id(), d);  // fire-and-forget reduction, no round trip
+#else
   if (S.flags & F_CLAIMS_CHANGED) {
     const uint32_t* r = S.cl[lane_id()];
     const uint32_t ne = (lane_id() < S.C && live_state(r[0] & 0xFFu) && r[CF_D] > 0)
@@ -2054,6 +2107,7 @@ __device__ __noinline__ void finish() {
   __syncwarp();
   const uint32_t d = S.ctr[lane_id()];
   if (d) atomicAdd(S.ctrp + lane_id(), d);  // fire-and-forget reduction, no round trip
+#endif
 }
 
 struct StepArgs {
