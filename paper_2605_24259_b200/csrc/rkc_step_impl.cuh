@@ -99,9 +99,10 @@ struct alignas(16) Warp {      // the warp's shared memory (one warp per CTA)
   uint32_t t, step, nv, NS, C, Q, O, EPT;
   uint32_t h[H_NWORDS];        // hot header
   uint32_t rq[8];              // the request record of the current op
-  alignas(16) uint32_t nev, flags, cdirty, pad0;  // one 16-B load in finish()
+  alignas(16) uint32_t nev;    // {nev, flags, cdirty, pad0}: one 16-B load in finish()
+  uint32_t flags, cdirty, pad0;
   uint32_t rc[4];              // objects whose blocks need reclassing
-  uint32_t objdirty[4];
+  alignas(16) uint32_t objdirty[4];
   uint32_t ctr[32];            // counter deltas of this step
   alignas(16) uint32_t cl[32][8];  // claim records (lane c owns claim c)
   uint32_t obj0[kObjMax];      // object word 0
@@ -117,6 +118,9 @@ struct alignas(16) Warp {      // the warp's shared memory (one warp per CTA)
 };
 
 static_assert(offsetof(Warp, cl) % 16 == 0, "uint4 access to claim rows");
+static_assert(offsetof(Warp, nev) % 16 == 0 && offsetof(Warp, flags) == offsetof(Warp, nev) + 4 &&
+              offsetof(Warp, cdirty) == offsetof(Warp, nev) + 8, "one 16-B load of {nev, flags, cdirty}");
+static_assert(offsetof(Warp, objdirty) % 16 == 0, "one 16-B load of objdirty");
 static_assert(offsetof(Warp, keys) % 16 == 0, "uint4 access to staged keys");
 __shared__ Warp S_[kWarpsPerCta];
 #define S (S_[kWarpsPerCta == 1 ? 0u : (threadIdx.x >> 5)])
@@ -606,16 +610,6 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
       break;
     }
     case JOB_RECLASS: {  // class bits of the marked objects' cached blocks (S.lim3 / S.lim2 / S.cnt3)
-#if RKC_RC_REGS
-      const uint32_t rcw0 = S.rc[0], rcw1 = S.rc[1], rcw2 = S.rc[2], rcw3 = S.rc[3];
-      auto in_rc = [&](uint32_t o) -> bool {
-        const uint32_t w = kObjMax <= 64 ? (o < 32 ? rcw0 : rcw1)
-                                         : (o < 64 ? (o < 32 ? rcw0 : rcw1) : (o < 96 ? rcw2 : rcw3));
-        return (w >> (o & 31u)) & 1u;
-      };
-#else
-      auto in_rc = [&](uint32_t o) -> bool { return in_reclass(o); };
-#endif
 #pragma unroll(kCrewUnroll)
       for (uint32_t j = j0; j < j1; ++j) {
         crew_pf(meta4, j, j1);
@@ -624,7 +618,7 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const uint32_t m = el(mv, e);
-          any |= meta_res(m) == kResCached && in_rc(meta_owner(m));
+          any |= meta_res(m) == kResCached && in_reclass(meta_owner(m));
         }
         if (!any) continue;
         const uint4 kv = __ldcg(key4 + j * 32 + lane);
@@ -633,7 +627,7 @@ __device__ __noinline__ void crew_work(uint32_t kind, uint32_t w) {
           const uint32_t m = el(mv, e);
           if (meta_res(m) != kResCached) continue;
           const uint32_t o = meta_owner(m);
-          if (!in_rc(o)) continue;
+          if (!in_reclass(o)) continue;
           const uint32_t pos = meta_pos(m);
           const bool pin = meta_pinned(m);  // shared by a running hit: class 3, not protected (G29)
           const uint32_t cls = (pin || pos < S.lim3[o]) ? 3u : (pos < S.lim2[o] ? 2u : 1u);
