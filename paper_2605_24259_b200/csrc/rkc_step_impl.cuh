@@ -62,7 +62,7 @@ constexpr int kCrewUnroll = RKC_CREW_UNROLL;  // block vectors in flight per lan
 constexpr uint32_t kObjMax = RKC_OMAX;
 
 #ifndef RKC_HDR_ALWAYS
-#define RKC_HDR_ALWAYS 0
+#define RKC_HDR_ALWAYS 1   // round 2: c5 -0.5 %
 #endif
 #ifndef RKC_FINISH_VEC
 #define RKC_FINISH_VEC 1   // round 2: c5 -1.4 %
