@@ -244,7 +244,16 @@ RKC_API rkc_status rkc_op_stage(rkc_pool* pool, const rkc_trace_op* ops, uint32_
  *                 (step-major).  on_device=0: host memory (copied through a
  *                 device staging buffer, pinned host memory overlaps the copy
  *                 with the steps).
- * Every step is one launch of the step kernel over all traces. */
+ * Every step is one light pass over all traces plus a step grid over the
+ * traces whose op needs a warp (pools of <= 1024 blocks: sized by the host
+ * from the heavy count the step published three steps earlier, read from a
+ * mapped pinned ring -- so in replay mode the call returns only when the
+ * device is about three steps from the end of the batch; a stream under graph
+ * capture, or a count that does not arrive within a second, falls back to the
+ * fixed 9/16 grid).  Results never depend on the grid: items past it run on
+ * an overflow kernel.  Errors: RKC_E_INVAL (NULL pool, num_steps != 1 with
+ * ops == NULL), RKC_E_STATE (staged ops pending), RKC_E_CUDA (the failing
+ * call is named on stderr). */
 RKC_API rkc_status rkc_step_batch(rkc_pool* pool, const rkc_op* ops, uint32_t num_steps, int on_device,
                           void* stream);
 
